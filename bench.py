@@ -1,0 +1,480 @@
+#!/usr/bin/env python
+"""METRO routing benchmark (BASELINE.json metric): µs per MoE layer incl. the
+all-gather, and max activated replicas per EP rank, METRO vs EPLB.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config ds] [--impl b200|reference]
+
+N > 1 is launched by the driver with torch.distributed.run (one rank per GPU,
+NCCL).  A step = one MoE layer: [NCCL all-gather of every rank's top-k ids] +
+the sm_100a METRO routing kernel over the global batch.  The global decode
+batch (B tokens) is fixed as N grows ("strong" scaling); every rank routes the
+whole batch (replicated, deterministic).  Inputs: pools of distinct synthetic
+batches resident in HBM; L2 is flushed (256 MiB memset) between steps outside
+the timed events.
+
+Rank 0 prints ONE JSON line.  --impl reference times the reference algorithm's
+CPU path (the oracle port, oracle/metro_oracle.c: aggregate_loads + route_metro +
+per-pair replica) on the host on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "METRO routing µs/MoE layer (incl. allGather); max activated replicas/GPU vs EPLB"
+
+CONFIGS = {
+    "ds": dict(workload="DeepSeek-V3 shape: 256 routed experts top-8, 8 EP ranks, 50% replication "
+                        "(EPLB placement), 1024 decode tokens", N=256, k=8, G=8, ratio=1.5, B=1024),
+    "q30": dict(workload="Qwen3-30B-A3B shape: 128 experts top-8, 8 EP ranks, 50% replication, "
+                         "256 decode tokens", N=128, k=8, G=8, ratio=1.5, B=256),
+    "q235_125": dict(workload="Qwen3-235B-A22B shape: 128 experts top-8, 16 logical EP ranks, 25% "
+                              "replication, 1024 decode tokens", N=128, k=8, G=16, ratio=1.25, B=1024),
+    "q235_150": dict(workload="Qwen3-235B-A22B shape, 50% replication", N=128, k=8, G=16, ratio=1.5, B=1024),
+    "q235_200": dict(workload="Qwen3-235B-A22B shape, 100% replication", N=128, k=8, G=16, ratio=2.0, B=1024),
+}
+for _b in (64, 128, 256, 512, 2048, 4096, 8192):
+    CONFIGS[f"ds_b{_b}"] = dict(workload=f"DeepSeek-V3 shape, decode batch {_b}", N=256, k=8, G=8,
+                                ratio=1.5, B=_b)
+
+POOL = 32          # distinct batches resident in HBM, cycled through the steps
+FLUSH_BYTES = 256 << 20
+SKEW = 1.2
+POP_SEED = 7
+
+
+def parse_args():
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--config", default="ds", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cluster", type=int, default=0, help="CTAs per routing cluster (0 = auto)")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU-baseline sample length")
+    ap.add_argument("--e2e-steps", type=int, default=1000)
+    ap.add_argument("--detail", default=None, help="write extra per-run detail JSON here")
+    return ap.parse_args()
+
+
+def workload(cfg, world: int):
+    from paper_2512_09277_b200.placement import gen_zipf_topk, make_placement
+
+    A = make_placement(cfg["N"], cfg["G"], cfg["ratio"], POP_SEED).matrix
+    batches = [gen_zipf_topk(cfg["N"], cfg["k"], cfg["B"], SKEW, 1000 + s, popularity_seed=POP_SEED)
+               for s in range(POOL)]
+    return A, batches
+
+
+def algorithmic_bytes(cfg) -> int:
+    """Per routing launch: read ids + rank masks; write loads,
+    choice, rank_counts, lam, status, pair_rank."""
+    pairs = cfg["B"] * cfg["k"]
+    w = (cfg["G"] + 31) // 32
+    return pairs * 4 + cfg["N"] * w * 4 + cfg["N"] * 4 * 2 + cfg["G"] * 4 + 4 + 16 + pairs * 4
+
+
+def load_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)", pk
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)", {}
+
+
+def load_traffic(cfg_name: str):
+    path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(cfg_name)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML SM clock + throttle reasons sampled from a thread during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period: float = 0.005):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period = period
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ CPU (oracle port)
+def cpu_route_layers(A, batches, seconds: float, min_layers: int = 0):
+    """Time the oracle port (aggregate_loads + route_metro + pair_rank) per layer on
+    one host core; returns (µs/layer, layers, outputs of the first len(batches))."""
+    import oracle
+
+    outs = [oracle.metro_layer(b, A) for b in batches]  # warm + results for the parity check
+    scratch = [tuple(np.copy(x) for x in o) for o in outs]
+    n, t0 = 0, time.perf_counter()
+    while True:
+        for i, b in enumerate(batches):
+            oracle.metro_layer(b, A, scratch[i])
+        n += len(batches)
+        el = time.perf_counter() - t0
+        if el >= seconds and n >= min_layers:
+            break
+    return el / n * 1e6, n, outs
+
+
+def cpu_allcores_throughput(A, batches, seconds: float = 2.0):
+    """Independent layers on every host core (context only; one layer is serial)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+
+    cores = len(os.sched_getaffinity(0))
+    oracle.lib()
+
+    def worker(_):
+        scratch = [oracle.metro_layer(b, A) for b in batches]
+        n, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < seconds:
+            for i, b in enumerate(batches):
+                oracle.metro_layer(b, A, scratch[i])
+            n += len(batches)
+        return n
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(cores) as ex:  # ctypes releases the GIL during the C call
+        total = sum(ex.map(worker, range(cores)))
+    return total / (time.perf_counter() - t0), cores
+
+
+def run_reference(args, cfg, rank: int, world: int):
+    if rank != 0:
+        return None
+    A, batches = workload(cfg, world)
+    import oracle
+
+    oracle.build()
+    for _ in range(args.warmup):
+        for b in batches[:4]:
+            oracle.metro_layer(b, A)
+    # each step: one layer = one batch of the same workload, on one host core
+    per = []
+    scratch = [oracle.metro_layer(b, A) for b in batches]
+    for s in range(args.steps):
+        b = batches[s % len(batches)]
+        t0 = time.perf_counter()
+        oracle.metro_layer(b, A, scratch[s % len(batches)])
+        per.append(time.perf_counter() - t0)
+    us = statistics.mean(per) * 1e6
+    thr, cores = cpu_allcores_throughput(A, batches, 1.0)
+    sample = (f"{args.steps} layers of the {args.config} workload (B={cfg['B']}, N={cfg['N']}, "
+              f"G={cfg['G']}), one layer per step, single thread")
+    return {
+        "impl": "reference", "metric": METRIC, "value": us, "unit": "us/layer", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": data_str(),
+        "config": config_dict(args, cfg, world),
+        "cpu_baseline": {"value": us, "unit": "us/layer", "cores": 1, "kind": "port", "sample": sample,
+                         "all_cores_layers_per_s": thr, "host_cores": cores},
+        "e2e": {"value": us, "unit": "us/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def data_str():
+    return ("synthetic: Zipf(1.2) expert popularity, top-8 distinct ids per token by Gumbel top-k; "
+            "EPLB placement from a Zipf history (reference generators, popularity seed 7)")
+
+
+def config_dict(args, cfg, world):
+    return {"workload": cfg["workload"], "name": args.config, "num_experts": cfg["N"], "top_k": cfg["k"],
+            "ep_ranks": cfg["G"], "replication": cfg["ratio"], "global_batch": cfg["B"],
+            "parallelism": f"ep all-gather over {world} GPU(s), routing replicated per rank",
+            "l2": "flushed between steps (256 MiB memset outside the timed events)",
+            "pool_batches": POOL}
+
+
+# ------------------------------------------------------------------ GPU
+def run_b200(args, cfg, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_09277_b200 import DevicePlacement, HostRouter, Router
+    from paper_2512_09277_b200.dist import DistributedRouter, allgather_topk
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    A, batches = workload(cfg, world)
+    B, k = cfg["B"], cfg["k"]
+    if B % world:
+        raise SystemExit(f"global batch {B} not divisible by {world} GPUs")
+    lt = B // world
+    pl = DevicePlacement(A, dev)
+    router = Router(pl, "metro", args.cluster)
+    eplb = Router(pl, "eplb", args.cluster)
+    # pools resident in HBM: this rank's shard of every batch, and the global batches
+    local_pool = [torch.from_numpy(b[rank * lt:(rank + 1) * lt].copy()).to(dev) for b in batches]
+    global_pool = [torch.from_numpy(b).to(dev) for b in batches]
+    gathered = torch.empty((B, k), dtype=torch.int32, device=dev)
+    out = router.alloc(B * k, top_k=k)
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    tick = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def step(i):
+        if world > 1:
+            allgather_topk(local_pool[i % POOL], gathered)
+            ids = gathered
+        else:
+            ids = global_pool[i % POOL]
+        return ids
+
+    # warm-up (also JIT-free: the .so is prebuilt)
+    for i in range(max(args.warmup, 3)):
+        router.route(step(i), out=out)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    with ClockSampler(local_rank) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        wall0 = time.perf_counter()
+        for i in range(K):
+            flush.zero_()
+            if world > 1:
+                dist.all_reduce(tick)  # device-side rank alignment before the timed events
+            ev[i][0].record()
+            ids = step(i)
+            ev[i][1].record()
+            router.route(ids, out=out)
+            ev[i][2].record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+        if world > 1:
+            dist.barrier()
+    step_ms = [ev[i][0].elapsed_time(ev[i][2]) for i in range(K)]
+    kern_ms = [ev[i][1].elapsed_time(ev[i][2]) for i in range(K)]
+    ag_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(K)]
+    mean_step = statistics.mean(step_ms)
+    mean_kern = statistics.mean(kern_ms)
+    mean_ag = statistics.mean(ag_ms)
+    if world > 1:
+        t = torch.tensor([mean_step, mean_kern, mean_ag], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        mean_step, mean_kern, mean_ag = t.tolist()
+
+    # graph-replayed and L2-warm figures (context)
+    g_us = None
+    if world == 1:
+        static = global_pool[0]
+        gr = torch.cuda.CUDAGraph()
+        router.route(static, out=out)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(gr):
+            for _ in range(20):
+                router.route(static, out=out)
+        gr.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            gr.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        g_us = e0.elapsed_time(e1) * 1e3 / 200
+
+    # lambda METRO vs EPLB over the pool (device outputs)
+    lam_m, lam_e = [], []
+    eout = eplb.alloc(B * k, pair_rank=False, top_k=k)
+    for b in global_pool:
+        router.route(b, out=out).check()
+        eplb.route(b, out=eout, pair_rank=False).check()
+        lam_m.append(int(out.lam.item()))
+        lam_e.append(int(eout.lam.item()))
+
+    # end to end from host buffers: H2D ids, route, D2H results, sync
+    e2e_us, h2d, d2h = None, 0, 0
+    E = min(args.e2e_steps, K)
+    if world == 1:
+        hr = HostRouter(pl, B * k, args.cluster)
+        hosts = [torch.from_numpy(b.reshape(-1).copy()).pin_memory() for b in batches]
+        prh = torch.empty(B * k, dtype=torch.int32).pin_memory()
+        for i in range(10):
+            hr(hosts[i % POOL], prh)
+        per = []
+        for i in range(E):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            hr(hosts[i % POOL], prh)
+            per.append(time.perf_counter() - t0)
+        e2e_us = statistics.mean(per) * 1e6
+        h2d = B * k * 4
+        d2h = (8 + cfg["G"] + cfg["N"]) * 4 + B * k * 4
+    else:
+        dr = DistributedRouter(pl, lt, k, "metro", args.cluster)
+        hosts = [torch.from_numpy(b[rank * lt:(rank + 1) * lt].copy()).pin_memory() for b in batches]
+        small_h = torch.empty(8 + cfg["G"] + cfg["N"], dtype=torch.int32).pin_memory()
+        own_h = torch.empty(lt * k, dtype=torch.int32).pin_memory()
+        small_d = torch.empty_like(small_h, device=dev)
+        per = []
+        for i in range(E + 10):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            dr.local.copy_(hosts[i % POOL].view(lt, k), non_blocking=True)
+            o = dr.step()
+            small_d[0:4].copy_(o.status)
+            small_d[4:5].copy_(o.lam)
+            small_d[8:8 + cfg["G"]].copy_(o.rank_counts)
+            small_d[8 + cfg["G"]:].copy_(o.choice)
+            small_h.copy_(small_d, non_blocking=True)
+            own_h.copy_(dr.own_pair_rank(), non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            if i >= 10:
+                per.append(time.perf_counter() - t0)
+        t = torch.tensor([statistics.mean(per)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_us = t.item() * 1e6
+        h2d = lt * k * 4
+        d2h = small_h.numel() * 4 + lt * k * 4
+
+    if rank != 0:
+        return None
+
+    peak, peak_src, _ = load_peaks()
+    alg = algorithmic_bytes(cfg)
+    achieved = alg / (mean_kern * 1e-3) / 1e9
+    res = {
+        "metric": METRIC, "value": mean_step * 1e3, "unit": "us/layer", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": mean_step, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int32", "data": data_str(),
+        "config": config_dict(args, cfg, world),
+        "e2e": {"value": e2e_us, "unit": "us/layer", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": K,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": load_traffic(args.config),
+                     "peak_source": peak_src, "algorithmic_bytes_per_launch": alg,
+                     "kernel": "metro_ids_kernel", "kernel_us": mean_kern * 1e3,
+                     "note": "latency-bound serial greedy; HBM fraction is low by construction"},
+        "breakdown_us": {"allgather": mean_ag * 1e3 if world > 1 else 0.0, "route_kernel": mean_kern * 1e3,
+                         "step_p50": float(np.percentile(step_ms, 50)) * 1e3,
+                         "step_p99": float(np.percentile(step_ms, 99)) * 1e3,
+                         "graph_replayed_l2_warm": g_us, "timed_wall_s": wall},
+        "lambda": {"metro_mean": statistics.mean(lam_m), "eplb_mean": statistics.mean(lam_e),
+                   "metro_max": max(lam_m), "eplb_max": max(lam_e),
+                   "metro_le_eplb_all": all(a <= b for a, b in zip(lam_m, lam_e)), "batches": len(lam_m)},
+        "clocks": clk.summary(),
+    }
+    if world > 1:
+        recv = (world - 1) * lt * k * 4
+        res["nvlink"] = {"allgather_recv_bytes_per_rank": recv,
+                         "achieved_gbs": recv / (mean_ag * 1e-3) / 1e9, "peak_gbs": 770.0,
+                         "frac": recv / (mean_ag * 1e-3) / 1e9 / 770.0,
+                         "peak_source": "measured peer copy, B200_PROFILING.md"}
+    if world == 1:
+        us, layers, outs = cpu_route_layers(A, batches, args.cpu_seconds)
+        parity = all(int(o[3][0]) == lm for o, lm in zip(outs, lam_m))
+        # full-output parity of the last routed batch (choice / counts / pair_rank)
+        router.route(global_pool[-1], out=out)
+        torch.cuda.synchronize()
+        o = outs[-1]
+        parity = parity and np.array_equal(out.choice.cpu().numpy(), o[1]) and \
+            np.array_equal(out.pair_rank.cpu().numpy(), o[4].reshape(-1))
+        thr, cores = cpu_allcores_throughput(A, batches, 1.0)
+        res["cpu_baseline"] = {
+            "value": us, "unit": "us/layer", "cores": 1, "kind": "port",
+            "sample": f"{layers} layers ({args.cpu_seconds:.0f} s) of this workload through the oracle "
+                      "port (aggregate_loads + route_metro + pair_rank), single thread",
+            "all_cores_layers_per_s": thr, "host_cores": cores, "parity_vs_gpu": bool(parity),
+        }
+    return res
+
+
+def main():
+    args = parse_args()
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        res = run_reference(args, cfg, rank, world)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        res = run_b200(args, cfg, rank, world, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+    if res is not None:
+        print(json.dumps(res))
+        if args.detail:
+            with open(args.detail, "w") as f:
+                json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

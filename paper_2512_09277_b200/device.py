@@ -1,0 +1,228 @@
+"""Device fast path: placement bitmasks resident in HBM, routing on CUDA tensors.
+
+This is the serving-side interface (what a MoE layer calls once per decode
+step): device-resident ``topk_ids`` in, device tensors out, stream-ordered, no
+host synchronisation, CUDA-graph capturable.  The reference-compatible numpy
+API in ``routing.py`` is a thin host wrapper over the same kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _native
+from .core import ValidationError
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(device: torch.device, stream: Optional[torch.cuda.Stream] = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return s.cuda_stream
+
+
+def _require_cuda(t: torch.Tensor, name: str, dtype: torch.dtype) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValidationError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValidationError(f"{name} must be {dtype}, got {t.dtype}")
+    return t.contiguous()
+
+
+def pack_placement(matrix) -> np.ndarray:
+    """Binary A[N, G] -> rank bitmasks [N, W] uint32 (C-ABI metro_pack_placement)."""
+    mat = np.ascontiguousarray(np.asarray(getattr(matrix, "matrix", matrix)))
+    if mat.ndim != 2:
+        raise ValidationError("placement matrix must be 2-dimensional")
+    if mat.dtype != np.int8:
+        if ((mat != 0) & (mat != 1)).any():
+            raise ValidationError("placement matrix must be binary")
+        mat = mat.astype(np.int8)
+    n, g = mat.shape
+    L = _native.lib()
+    w = max(1, L.metro_mask_words(max(g, 1)))
+    mask = np.zeros((n, w), dtype=np.uint32)
+    rc = L.metro_pack_placement(mat.ctypes.data, n, g, mask.ctypes.data)
+    if rc == _native.ENOTBINARY:
+        raise ValidationError("placement matrix must be binary")
+    _native.check_rc(rc, "metro_pack_placement")
+    return mask
+
+
+class DevicePlacement:
+    """One layer's EPLB placement as per-expert rank bitmasks in HBM.
+
+    Uploaded once per rebalance window (cold path, reference placement.py:83-128
+    builds A); every routing launch reads N * W * 4 bytes of it.
+    """
+
+    def __init__(self, A, device=None):
+        mat = np.asarray(getattr(A, "matrix", A))
+        if mat.ndim != 2:
+            raise ValidationError("placement matrix must be 2-dimensional")
+        n, g = mat.shape
+        if not (1 <= n <= _native.MAX_N and 1 <= g <= _native.MAX_G):
+            raise ValidationError(
+                f"placement {n}x{g} outside the sm_100a kernel limits "
+                f"(1 <= N <= {_native.MAX_N}, 1 <= G <= {_native.MAX_G})"
+            )
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        mask = pack_placement(mat)
+        self.num_experts, self.num_ranks, self.words = n, g, mask.shape[1]
+        self.mask_host = mask
+        self.mask = torch.from_numpy(mask.view(np.int32)).to(self.device)
+        self.replica_counts = np.asarray(mat != 0).sum(axis=1)
+
+
+@dataclass
+class RouteResult:
+    """Device outputs of one routing launch (all int32 CUDA tensors).
+
+    loads[N]; choice[N] (METRO; -1 inactive) or x[N, G] (EPLB); rank_counts[G];
+    lam[1]; pair_rank[num_pairs] (optional); status[4] (see metro_route.h).
+    """
+
+    kind: str
+    loads: Optional[torch.Tensor]
+    choice: Optional[torch.Tensor]
+    x: Optional[torch.Tensor]
+    rank_counts: torch.Tensor
+    lam: torch.Tensor
+    pair_rank: Optional[torch.Tensor]
+    status: torch.Tensor
+    top_k: int = 1
+
+    def check(self) -> "RouteResult":
+        """Synchronise on status and raise the reference's exception on error."""
+        raise_status(self.status.cpu().numpy(), self.top_k)
+        return self
+
+
+def raise_status(status: np.ndarray, top_k: int = 1) -> None:
+    code = int(status[0])
+    if code == _native.OK:
+        return
+    if code == _native.ERR_ID_RANGE:
+        pair = int(np.uint32(status[1])) | (int(np.uint32(status[2])) << 32)
+        raise ValidationError(f"token {pair // max(top_k, 1)}: expert id {int(status[3])} out of range")
+    if code == _native.ERR_NO_REPLICA:
+        # reference: `assert gpus` / `assert best >= 0` (routing.py:66, :99)
+        raise AssertionError("placement invariant: every expert has a replica")
+    if code == _native.ERR_LOAD_RANGE:
+        raise ValidationError("load does not fit the device loads path")
+    raise _native.NativeLibraryError(f"unknown kernel status {code}")
+
+
+class Router:
+    """Routes device-resident top-k ids against one DevicePlacement.
+
+    ``kind`` is ``"metro"`` (routing.py:105-113) or ``"eplb"`` (routing.py:55-72).
+    ``cluster_ctas`` = CTAs in the thread-block cluster (0 = auto by batch size).
+    """
+
+    KINDS = ("metro", "eplb")
+
+    def __init__(self, placement: DevicePlacement, kind: str = "metro", cluster_ctas: int = 0):
+        if kind not in self.KINDS:
+            raise ValidationError(f"unknown device router kind {kind!r}; expected one of {self.KINDS}")
+        self.placement = placement
+        self.kind = kind
+        self.cluster_ctas = int(cluster_ctas)
+
+    def alloc(self, num_pairs: int, pair_rank: bool = True, with_x: bool = False, top_k: int = 1) -> RouteResult:
+        dev = self.placement.device
+        n, g = self.placement.num_experts, self.placement.num_ranks
+        i32 = dict(dtype=torch.int32, device=dev)
+        return RouteResult(
+            kind=self.kind,
+            loads=torch.empty(n, **i32),
+            choice=torch.empty(n, **i32) if self.kind == "metro" else None,
+            x=torch.empty((n, g), **i32) if (self.kind == "eplb" and with_x) else None,
+            rank_counts=torch.empty(g, **i32),
+            lam=torch.empty(1, **i32),
+            pair_rank=torch.empty(num_pairs, **i32) if pair_rank else None,
+            status=torch.zeros(4, **i32),
+            top_k=top_k,
+        )
+
+    def route(self, topk_ids: torch.Tensor, out: Optional[RouteResult] = None, pair_rank: bool = True,
+              with_x: bool = False, stream: Optional[torch.cuda.Stream] = None) -> RouteResult:
+        """Launch one routing kernel on ``stream`` (default: current stream)."""
+        ids = _require_cuda(topk_ids, "topk_ids", torch.int32)
+        top_k = ids.shape[-1] if ids.dim() >= 2 else 1
+        num_pairs = ids.numel()
+        if out is None:
+            out = self.alloc(num_pairs, pair_rank=pair_rank, with_x=with_x, top_k=top_k)
+        L = _native.lib()
+        p = self.placement
+        s = _stream(p.device, stream)
+        if self.kind == "metro":
+            rc = L.metro_route_v1(
+                ids.data_ptr(), num_pairs, p.mask.data_ptr(), p.num_experts, p.num_ranks,
+                _ptr(out.loads), out.choice.data_ptr(), out.rank_counts.data_ptr(), out.lam.data_ptr(),
+                _ptr(out.pair_rank), out.status.data_ptr(), self.cluster_ctas, s,
+            )
+        else:
+            rc = L.eplb_route_v1(
+                ids.data_ptr(), num_pairs, p.mask.data_ptr(), p.num_experts, p.num_ranks,
+                _ptr(out.loads), _ptr(out.x), out.rank_counts.data_ptr(), out.lam.data_ptr(),
+                _ptr(out.pair_rank), out.status.data_ptr(), self.cluster_ctas, s,
+            )
+        _native.check_rc(rc, f"{self.kind}_route_v1")
+        return out
+
+
+def aggregate_loads_device(topk_ids: torch.Tensor, num_experts: int, cluster_ctas: int = 0,
+                           stream: Optional[torch.cuda.Stream] = None):
+    """T[N] int32 on device + status[4] (metro_aggregate_loads_v1)."""
+    ids = _require_cuda(topk_ids, "topk_ids", torch.int32)
+    loads = torch.empty(num_experts, dtype=torch.int32, device=ids.device)
+    status = torch.zeros(4, dtype=torch.int32, device=ids.device)
+    rc = _native.lib().metro_aggregate_loads_v1(
+        ids.data_ptr(), ids.numel(), num_experts, loads.data_ptr(), status.data_ptr(), cluster_ctas,
+        _stream(ids.device, stream),
+    )
+    _native.check_rc(rc, "metro_aggregate_loads_v1")
+    return loads, status
+
+
+class HostRouter:
+    """End-to-end METRO from host (pinned) buffers through metro_route_host_v1.
+
+    Each call: H2D of the ids, the routing kernel, D2H of choice / rank_counts /
+    lam / status (+ pair_rank), stream synchronise -- the reference-facing call a
+    CPU-resident caller makes.
+    """
+
+    def __init__(self, placement: DevicePlacement, max_pairs: int, cluster_ctas: int = 0):
+        self.placement = placement
+        self.cluster_ctas = int(cluster_ctas)
+        L = _native.lib()
+        n, g = placement.num_experts, placement.num_ranks
+        nbytes = L.metro_host_workspace_bytes(max_pairs, n, g)
+        self.max_pairs = max_pairs
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=placement.device)
+        self.host_out = torch.empty(8 + g + n, dtype=torch.int32).pin_memory()
+        self.stream = torch.cuda.Stream(placement.device)
+
+    def __call__(self, ids_host: torch.Tensor, pair_rank_host: Optional[torch.Tensor] = None) -> np.ndarray:
+        if ids_host.is_cuda or ids_host.dtype != torch.int32 or not ids_host.is_contiguous():
+            raise ValidationError("ids_host must be a contiguous int32 CPU tensor (pinned for speed)")
+        if ids_host.numel() > self.max_pairs:
+            raise ValidationError("batch larger than the HostRouter workspace")
+        p = self.placement
+        rc = _native.lib().metro_route_host_v1(
+            ids_host.data_ptr(), ids_host.numel(), p.mask.data_ptr(), p.num_experts, p.num_ranks,
+            self.ws.data_ptr(), self.host_out.data_ptr(),
+            None if pair_rank_host is None else pair_rank_host.data_ptr(), self.cluster_ctas,
+            self.stream.cuda_stream,
+        )
+        _native.check_rc(rc, "metro_route_host_v1")
+        return self.host_out.numpy()
