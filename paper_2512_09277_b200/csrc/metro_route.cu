@@ -7,24 +7,30 @@
 //     _greedy_assign routing.py:90-102  argmin L over ascending replicas, strict '<'
 //   route_eplb       routing.py:55-72   even split, remainder to low rank ids
 //
-// Kernel structure: one thread-block cluster of R CTAs routes one
-// layer.  Every CTA
-//   (A) stages its contiguous slice of the all-gathered top-k ids in shared memory
-//       with one TMA bulk copy (cp.async.bulk + mbarrier), the rank bitmasks likewise;
-//   (B) histograms the slice (lane-striped shared counters -> conflict-free);
-//   (C) pushes its partial histogram into every CTA's shared memory over DSMEM and
-//       passes ONE cluster barrier;
-//   (D) redundantly (so no second barrier is needed) sums the partials into T,
-//       applies the order-free forced prefix (experts with one replica) with
-//       warp ballots, compacts + rank-sorts the replicated active experts by the
-//       canonical key, and runs the serial greedy in ONE warp: lane g owns
-//       counter L[g]; each step is a redux.sync min over (L << 8 | g) of the
-//       candidate lanes, which is exactly "smallest L, lowest rank id on ties";
-//   (E) writes pair_rank for its own slice from shared memory (ids never re-read
-//       from HBM); CTA 0 writes loads / choice / rank_counts / lam / status.
+// Kernel structure.  One thread-block cluster of R CTAs routes
+// one layer; the path is a latency chain, so every phase is shaped to keep
+// memory latency off it:
+//   (A) thread 0 issues the TMA bulk copies (cp.async.bulk + mbarrier) of the rank
+//       bitmasks and of this CTA's contiguous id slice as its first instruction;
+//   (B) the slice is histogrammed into lane-striped shared counters hist[e][lane]
+//       (each lane owns a bank: hot experts never serialise a warp's atomics);
+//   (C) each expert's 32 lane counters are summed with bank-rotated 128-bit loads
+//       and the partial is stored straight into every peer CTA's shared memory
+//       (DSMEM st.shared::cluster) -- ONE cluster barrier completes the exchange;
+//   (D) every CTA redundantly (no second barrier) sums the partials into T and
+//       classifies experts in the same pass: single-replica experts are applied
+//       as an order-free prefix (per-rank ballots), replicated ones are
+//       stream-compacted, rank-sorted by the canonical key with broadcast loads,
+//       and the serial greedy runs in ONE warp: lane g owns L[g] packed as
+//       (L << 8 | g); the candidacy bits of 32 steps are transposed into
+//       registers with ballots, so each step is SEL -> redux.sync.min -> compare ->
+//       add with no memory access on the dependency chain;
+//   (E) each CTA writes pair_rank for its own slice from shared memory; CTA 0
+//       writes loads / choice / rank_counts / lam / status.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -41,8 +47,10 @@ constexpr int kMaxN = 4096;
 constexpr int kMaxCluster = 16;
 constexpr int kMaxSmem = 232448;  // 227 KB opt-in on sm_100
 constexpr int64_t kNoBad = INT64_MAX;
+constexpr uint32_t kBadLo = 0xffffffffu, kBadHi = 0x7fffffffu;  // kNoBad split
 
 enum Kind { kMetroIds = 0, kEplbIds = 1, kMetroLoads = 2, kEplbLoads = 3, kMetroOrdered = 4 };
+enum Mode { kFromIds = 0, kFromLoads = 1, kFromOrder = 2 };
 
 struct Params {
     const int32_t *ids;
@@ -67,14 +75,17 @@ struct Params {
 
 // ---------------------------------------------------------------- smem layout
 // mbar | misc | mask | ids (staged slice) | T | choice | aux | hist | part
-// The METRO decide scratch (keys, cand, sorted) aliases hist + part: both are
-// dead once the partial histograms have been reduced into T.
+// The METRO sort/greedy scratch (keys, cand, smask, sid) aliases hist + part:
+// both are dead once the partial histograms have been reduced into T.
 struct Layout {
-    int mbar, misc, mask, ids, T, choice, aux, hist, part, keys, cand, sorted, total;
+    int mbar, misc, mask, ids, T, choice, aux, hist, part, keys, cand, smask, sid, ent, total;
     int NP;  // partial-row stride (words): N + 2 (bad pair lo/hi) rounded to 4
 };
 
 __host__ __device__ inline int align_up(int x, int a) { return (x + a - 1) / a * a; }
+
+// packed greedy entry sizes (words): r = 2 / r = 3 / generic
+constexpr int kE2 = 8, kE3 = 12, kEG = 12;
 
 __host__ __device__ inline Layout make_layout(int kind, int N, int W, int R, int64_t slice,
                                               int C, int staged, bool warp_hist = false) {
@@ -90,49 +101,46 @@ __host__ __device__ inline Layout make_layout(int kind, int N, int W, int R, int
     if (ids_mode && staged) o = align_up(o + (int)slice * 4, 16);
     L.T = o; o = align_up(o + N * (kind == kEplbIds ? 8 : 4), 16);  // EPLB: + CTA base
     L.choice = o;
-    if (metro) o = align_up(o + N * 4, 16);
-    L.aux = o; o = align_up(o + kMaxG * 4, 16);  // forced counts L0 / EPLB rank counts
+    if (metro) o = align_up(o + (N + 4) * 4, 16);  // + dummy slot for padded entries
+    L.aux = o; o = align_up(o + 2 * kMaxG * 4, 16);  // L0 / EPLB counts | active-per-rank
     L.hist = o;
     int hist_bytes = 0;
     if (ids_mode) hist_bytes = warp_hist ? kWarps * N * 4 : N * C * 4;
     L.part = align_up(o + hist_bytes, 16);
     const int end1 = ids_mode ? align_up(L.part + R * L.NP * 4, 16) : L.part;
     L.keys = o;
-    L.cand = align_up(L.keys + N * 8, 16);
-    L.sorted = align_up(L.cand + N * 4, 16);
-    const int end2 = metro ? align_up(L.sorted + N * (W + 1) * 4, 16) : o;
+    L.cand = align_up(L.keys + (N + 8) * 8, 16);
+    L.smask = align_up(L.cand + N * 4, 16);
+    L.sid = align_up(L.smask + N * W * 4, 16);
+    L.ent = align_up(L.sid + N * 4, 16);
+    // packed-greedy entries (W == 1 only): r=2, r=3 and generic arrays, padded by 4
+    const int end2 = metro ? align_up(L.ent + (W == 1 ? (N + 16) * kE3 * 4 : 0), 16) : o;
     L.total = end1 > end2 ? end1 : end2;
     return L;
 }
 
 // misc word indices
 enum {
-    M_BAD_LO = 0, M_BAD_HI = 1,   // int64 min bad pair (local)
-    M_NOREP = 2,                  // min active expert without replica
-    M_M2 = 3,                     // number of replicated active experts
-    M_LOADERR = 4,
-    M_ANY = 5,
-    M_BADALL_LO = 6, M_BADALL_HI = 7,
-    M_WCNT = 16,                  // [kWarps] per-warp compaction counts
+    M_BAD_LO = 0, M_BAD_HI = 1,        // this CTA's min bad pair index (int64)
+    M_NOREP = 2,                       // min active expert without replica
+    M_LOADERR = 3,
+    M_BADALL_LO = 4, M_BADALL_HI = 5,  // cluster-wide min bad pair index
+    M_M2 = 6,                          // replicated active experts (compaction cursor)
+    M_N2 = 7, M_N3 = 8,                // of which r == 2 / r == 3
 };
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-                 : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
-
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
-
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
     asm volatile(
         "{\n\t.reg .pred P;\n"
@@ -142,17 +150,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
         "r"(phase)
         : "memory");
 }
-
 // TMA bulk copy global -> own shared memory, completion on the mbarrier.
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
-                                         uint64_t *bar) {
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
-        "[%3];" ::"r"(smem_u32(dst)),
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
-
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -172,256 +177,113 @@ __device__ __forceinline__ void cluster_arrive_release() {
 __device__ __forceinline__ void cluster_wait() {
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// Store 16 bytes into CTA `cta`'s shared memory at the address `local` has in ours.
-__device__ __forceinline__ void dsmem_st_v4(const void *local, uint32_t cta, uint4 v) {
+// Store one word into CTA `cta`'s shared memory at the address `local` has in ours.
+__device__ __forceinline__ void dsmem_st(const void *local, uint32_t cta, uint32_t v) {
     uint32_t raddr;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(local)), "r"(cta));
-    asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(raddr), "r"(v.x),
-                 "r"(v.y), "r"(v.z), "r"(v.w)
-                 : "memory");
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(raddr), "r"(v) : "memory");
 }
-
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
     return m;
 }
-
 __device__ __forceinline__ void stamp(const Params &p, int i) {
     if (p.stamps && threadIdx.x == 0 && cluster_ctarank() == 0) p.stamps[i] = clock64();
 }
+__device__ __forceinline__ int64_t join64(uint32_t lo, uint32_t hi) {
+    return static_cast<int64_t>((static_cast<uint64_t>(hi) << 32) | lo);
+}
 
-// position of the (q+1)-th set bit of a W-word mask (q < popcount)
+// position of the (q+1)-th set bit of a W-word mask (q < popcount); short loops:
+// q < r <= G and r is 2..3 in practice
 template <int W>
 __device__ __forceinline__ int nth_set_bit(const uint32_t *mw, int q) {
 #pragma unroll
     for (int j = 0; j < W; ++j) {
-        int c = __popc(mw[j]);
-        if (q < c) return 32 * j + (int)__fns(mw[j], 0, q + 1);
+        const int c = __popc(mw[j]);
+        if (q < c) {
+            uint32_t m = mw[j];
+            for (int i = 0; i < q; ++i) m &= m - 1;
+            return 32 * j + __ffs(m) - 1;
+        }
         q -= c;
     }
     return -1;
 }
 
 // ---------------------------------------------------------------- phase A
-// Stage rank masks (+ this CTA's id slice) into shared memory with TMA bulk copies.
+struct StagePlan {
+    int mask_words;
+    bool mask_bulk, ids_bulk;
+    int body;
+};
+
 template <int W>
-__device__ void stage_inputs(const Params &p, const Layout &L, unsigned char *smem,
-                             int64_t beg, int n_local, bool stage_ids) {
+__device__ __forceinline__ StagePlan stage_plan(const Params &p, int64_t beg, int n_local, bool stage_ids) {
+    StagePlan s;
+    s.mask_words = p.mask ? p.N * W : 0;  // aggregate-only launches carry no mask
+    s.mask_bulk = s.mask_words > 0 && ((reinterpret_cast<uintptr_t>(p.mask) & 15) == 0) && (s.mask_words % 4 == 0);
+    s.body = stage_ids ? (n_local & ~3) : 0;
+    s.ids_bulk = stage_ids && s.body > 0 && ((reinterpret_cast<uintptr_t>(p.ids + beg) & 15) == 0);
+    return s;
+}
+
+// thread 0, first thing in the kernel: arm the mbarrier and launch the TMA copies
+__device__ __forceinline__ void stage_issue(const Params &p, const Layout &L, unsigned char *smem, int64_t beg,
+                                            const StagePlan &s) {
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + L.mbar);
+    mbar_init(bar, 1);
+    const uint32_t bytes = (s.mask_bulk ? s.mask_words * 4u : 0u) + (s.ids_bulk ? s.body * 4u : 0u);
+    mbar_arrive_expect_tx(bar, bytes);
+    if (s.mask_bulk) bulk_g2s(smem + L.mask, p.mask, s.mask_words * 4u, bar);
+    if (s.ids_bulk) bulk_g2s(smem + L.ids, p.ids + beg, s.body * 4u, bar);
+}
+
+// all threads: whatever the TMA could not take (unaligned / ragged tail)
+__device__ __forceinline__ void stage_rest(const Params &p, const Layout &L, unsigned char *smem, int64_t beg,
+                                           int n_local, bool stage_ids, const StagePlan &s) {
     uint32_t *s_mask = reinterpret_cast<uint32_t *>(smem + L.mask);
     int32_t *s_ids = reinterpret_cast<int32_t *>(smem + L.ids);
-    const int mask_words = p.mask ? p.N * W : 0;  // aggregate-only launches carry no mask
-    const bool mask_bulk = mask_words > 0 && ((reinterpret_cast<uintptr_t>(p.mask) & 15) == 0) &&
-                           (mask_words % 4 == 0);
-    const int body = stage_ids ? (n_local & ~3) : 0;
-    const bool ids_bulk =
-        stage_ids && body > 0 && ((reinterpret_cast<uintptr_t>(p.ids + beg) & 15) == 0);
-    if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        uint32_t bytes = (mask_bulk ? mask_words * 4u : 0u) + (ids_bulk ? body * 4u : 0u);
-        mbar_arrive_expect_tx(bar, bytes);
-        if (mask_bulk) bulk_g2s(s_mask, p.mask, mask_words * 4u, bar);
-        if (ids_bulk) bulk_g2s(s_ids, p.ids + beg, body * 4u, bar);
-    }
-    if (!mask_bulk)
-        for (int i = threadIdx.x; i < mask_words; i += kThreads) s_mask[i] = __ldg(p.mask + i);
-    if (stage_ids) {
-        const int from = ids_bulk ? body : 0;
-        for (int i = from + threadIdx.x; i < n_local; i += kThreads) s_ids[i] = __ldg(p.ids + beg + i);
-    }
-    __syncthreads();  // mbarrier init visible before anyone waits
-    mbar_wait(bar, 0);
+    if (!s.mask_bulk)
+        for (int i = threadIdx.x; i < s.mask_words; i += kThreads) s_mask[i] = __ldg(p.mask + i);
+    if (stage_ids)
+        for (int i = (s.ids_bulk ? s.body : 0) + threadIdx.x; i < n_local; i += kThreads)
+            s_ids[i] = __ldg(p.ids + beg + i);
 }
 
-// ---------------------------------------------------------------- phase D (METRO)
-// Given s_T (int32 loads, all CTAs), compute choice for every expert, run the
-// forced prefix + canonical sort + warp greedy.  Returns false on error
-// (status written by the writer CTA).
-template <int W>
-__device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *smem, bool writer,
-                             bool from_order) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int N = p.N, G = p.G;
-    int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
-    const uint32_t *s_mask = reinterpret_cast<const uint32_t *>(smem + L.mask);
-    const uint32_t *s_T = reinterpret_cast<const uint32_t *>(smem + L.T);
-    int32_t *s_choice = reinterpret_cast<int32_t *>(smem + L.choice);
-    uint64_t *s_keys = reinterpret_cast<uint64_t *>(smem + L.keys);
-    int32_t *s_cand = reinterpret_cast<int32_t *>(smem + L.cand);
-    uint32_t *s_sorted = reinterpret_cast<uint32_t *>(smem + L.sorted);
-    int32_t *s_L0 = reinterpret_cast<int32_t *>(smem + L.aux);
-
-    int m2 = 0;
-    if (!from_order) {
-        // ---- classify experts: inactive / forced (r == 1) / replicated (r >= 2)
-        for (int base = 0; base < N; base += kThreads) {
-            const int e = base + tid;
-            const bool valid = e < N;
-            uint32_t t = valid ? s_T[e] : 0u;
-            uint32_t mw[W];
-            int r = 0;
-#pragma unroll
-            for (int j = 0; j < W; ++j) {
-                mw[j] = valid ? s_mask[e * W + j] : 0u;
-                r += __popc(mw[j]);
-            }
-            const bool active = t > 0;
-            if (active && r == 0) atomicMin(&misc[M_NOREP], e);
-            const bool forced = active && r == 1;
-            const bool multi = active && r >= 2;
-            int g1 = -1;
-            if (forced) g1 = nth_set_bit<W>(mw, 0);
-            if (valid) s_choice[e] = forced ? g1 : -1;
-            // forced prefix: per-rank count of single-replica active experts.  The
-            // order among them is irrelevant: each lands on its
-            // only replica.  One shared atomic per distinct rank per warp.
-            unsigned rem = __ballot_sync(kFull, forced);
-            while (rem) {
-                const int leader = __ffs(rem) - 1;
-                const int gg = __shfl_sync(kFull, g1, leader);
-                const unsigned m = __ballot_sync(kFull, forced && g1 == gg);
-                if (lane == leader) atomicAdd(&s_L0[gg], __popc(m));
-                rem &= ~m;
-            }
-            // stream-compact replicated active experts (ascending id)
-            const unsigned bm = __ballot_sync(kFull, multi);
-            if (lane == 0) misc[M_WCNT + warp] = __popc(bm);
-            __syncthreads();
-            int off = m2, tot = 0;
-#pragma unroll
-            for (int w = 0; w < kWarps; ++w) {
-                const int c = misc[M_WCNT + w];
-                off += (w < warp) ? c : 0;
-                tot += c;
-            }
-            off += __popc(bm & lanemask_lt());
-            if (multi) {
-                // canonical key (routing.py:84-86): r asc, T desc, id asc
-                s_keys[off] = (static_cast<uint64_t>(r) << 56) |
-                              (static_cast<uint64_t>(0xffffffffu - t) << 24) |
-                              static_cast<uint64_t>(e);
-                s_cand[off] = e;
-            }
-            m2 += tot;
-            __syncthreads();
-        }
-        if (misc[M_NOREP] != INT32_MAX) {
-            if (writer && tid == 0) {
-                p.status[0] = METRO_ERR_NO_REPLICA;
-                p.status[1] = misc[M_NOREP];
-                p.status[2] = 0;
-                p.status[3] = 0;
-            }
-            return false;
-        }
-        stamp(p, 4);
-        // ---- rank-by-count sort of the m2 keys (distinct: ids are unique)
-        for (int c = warp; c < m2; c += kWarps) {
-            const uint64_t kc = s_keys[c];
-            int cnt = 0;
-            for (int c2 = lane; c2 < m2; c2 += 32) cnt += (s_keys[c2] < kc) ? 1 : 0;
-            cnt = __reduce_add_sync(kFull, cnt);
-            const int e = s_cand[c];
-            if (lane < W) s_sorted[cnt * (W + 1) + lane] = s_mask[e * W + lane];
-            if (lane == W) s_sorted[cnt * (W + 1) + W] = static_cast<uint32_t>(e);
-        }
-    } else {
-        // ---- caller-supplied order (metro-parallel): every listed expert goes
-        // through the greedy, single-replica ones included (no forced prefix).
-        m2 = p.order_len;
-        for (int s = tid; s < m2; s += kThreads) {
-            const int e = p.order[s];
-            int r = 0;
-            if (e >= 0 && e < N) {
-#pragma unroll
-                for (int j = 0; j < W; ++j) {
-                    const uint32_t w = s_mask[e * W + j];
-                    s_sorted[s * (W + 1) + j] = w;
-                    r += __popc(w);
-                }
-                s_sorted[s * (W + 1) + W] = static_cast<uint32_t>(e);
-            }
-            if (e < 0 || e >= N || r == 0) atomicMin(&misc[M_NOREP], (e < 0 || e >= N) ? -1 : e);
-        }
-        for (int e = tid; e < N; e += kThreads) s_choice[e] = -1;
-        __syncthreads();
-        if (misc[M_NOREP] != INT32_MAX) {
-            if (writer && tid == 0) {
-                p.status[0] = METRO_ERR_NO_REPLICA;
-                p.status[1] = misc[M_NOREP];
-                p.status[2] = 0;
-                p.status[3] = 0;
-            }
-            return false;
-        }
+__device__ __forceinline__ void init_misc(int32_t *misc) {
+    if (threadIdx.x < 64) {
+        const int i = threadIdx.x;
+        int32_t v = 0;
+        if (i == M_BAD_LO || i == M_BADALL_LO) v = static_cast<int32_t>(kBadLo);
+        if (i == M_BAD_HI || i == M_BADALL_HI) v = static_cast<int32_t>(kBadHi);
+        if (i == M_NOREP) v = INT32_MAX;
+        misc[i] = v;
     }
-    __syncthreads();
-    stamp(p, 5);
-
-    // ---- serial greedy (routing.py:94-101) in warp 0.
-    // lane owns ranks g = lane + 32 j; packed key (L << 8 | g): the warp-wide
-    // min over candidate lanes is "smallest L, then smallest g" -- the
-    // reference's ascending scan with strict '<'.
-    if (warp == 0) {
-        uint32_t Lk[W];
-#pragma unroll
-        for (int j = 0; j < W; ++j) {
-            const int g = lane + 32 * j;
-            Lk[j] = (g < G) ? ((static_cast<uint32_t>(s_L0[g]) << 8) | static_cast<uint32_t>(g))
-                            : 0xffffffffu;
-        }
-#pragma unroll 4
-        for (int s = 0; s < m2; ++s) {
-            const uint32_t *ent = s_sorted + s * (W + 1);
-            uint32_t v = 0xffffffffu;
-#pragma unroll
-            for (int j = 0; j < W; ++j) {
-                const uint32_t mw = ent[j];
-                v = ((mw >> lane) & 1u) ? min(v, Lk[j]) : v;
-            }
-            const uint32_t win = __reduce_min_sync(kFull, v);
-#pragma unroll
-            for (int j = 0; j < W; ++j) Lk[j] += (Lk[j] == win) ? 256u : 0u;
-            if (lane == 0) s_choice[ent[W]] = static_cast<int32_t>(win & 0xffu);
-        }
-        uint32_t mx = 0;
-#pragma unroll
-        for (int j = 0; j < W; ++j) {
-            const int g = lane + 32 * j;
-            if (g < G) {
-                const uint32_t c = Lk[j] >> 8;
-                if (writer) p.rank_counts[g] = static_cast<int32_t>(c);
-                mx = max(mx, c);
-            }
-        }
-        mx = __reduce_max_sync(kFull, mx);
-        if (writer && lane == 0) *p.lam = static_cast<int32_t>(mx);
-    }
-    __syncthreads();
-    stamp(p, 6);
-    return true;
 }
 
-// ---------------------------------------------------------------- histogram + exchange
-// Phase B + C for the ids kernels.  On return s_T holds the global loads and
-// (EPLB) s_T[N + e] holds this CTA's exclusive base (sum of earlier CTAs).
-template <int W, bool PRIV, bool BASE>
-__device__ bool histogram_exchange(const Params &p, const Layout &L, unsigned char *smem,
-                                   int64_t beg, int n_local, uint32_t R, uint32_t rank) {
+__device__ __forceinline__ void zero_smem(unsigned char *smem, int from, int to) {
+    for (int i = from / 16 + threadIdx.x; i < to / 16; i += kThreads)
+        reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0, 0, 0, 0);
+}
+
+// ---------------------------------------------------------------- phase B + C
+// Histogram this CTA's slice, then push the per-expert partial (and the CTA's
+// min bad pair index) into row `rank` of every CTA's partial table.  Ends with
+// the cluster barrier; afterwards part[r][e] holds CTA r's count of expert e.
+template <bool PRIV>
+__device__ void histogram_push(const Params &p, const Layout &L, unsigned char *smem, int64_t beg, int n_local,
+                               uint32_t R, uint32_t rank) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int N = p.N;
     int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
-    const int32_t *s_ids = reinterpret_cast<const int32_t *>(smem + L.ids);
     int32_t *s_hist = reinterpret_cast<int32_t *>(smem + L.hist);
     int32_t *s_part = reinterpret_cast<int32_t *>(smem + L.part);
-    uint32_t *s_T = reinterpret_cast<uint32_t *>(smem + L.T);
-    const int32_t *src = p.staged ? s_ids : (p.ids + beg);
+    const int32_t *src = p.staged ? reinterpret_cast<const int32_t *>(smem + L.ids) : (p.ids + beg);
     int64_t my_bad = kNoBad;
 
     if (!PRIV) {
-        // lane-striped counters hist[e][lane % C]: within one warp instruction every
-        // lane hits its own bank, so hot experts do not serialise the atomics.
         const int cm = p.C - 1;
         const int n4 = n_local & ~3;
         const bool vec = p.staged || ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
@@ -448,8 +310,8 @@ __device__ bool histogram_exchange(const Params &p, const Layout &L, unsigned ch
         }
     } else {
         // warp-private histograms over contiguous warp sub-slices; match_any groups
-        // equal ids so one lane does a plain read-modify-write.  The same walk
-        // later yields deterministic row-major occurrence ranks (EPLB pair_rank).
+        // equal ids so one lane does a plain read-modify-write.  The same walk later
+        // yields deterministic row-major occurrence ranks (EPLB pair_rank).
         const int ws = align_up((n_local + kWarps - 1) / kWarps, 32);
         const int wb = min(n_local, warp * ws), we = min(n_local, wb + ws);
         int32_t *hw = s_hist + warp * N;
@@ -466,124 +328,577 @@ __device__ bool histogram_exchange(const Params &p, const Layout &L, unsigned ch
         }
     }
     if (my_bad != kNoBad)
-        atomicMin(reinterpret_cast<unsigned long long *>(&misc[M_BAD_LO]),
-                  static_cast<unsigned long long>(my_bad));
+        atomicMin(reinterpret_cast<unsigned long long *>(&misc[M_BAD_LO]), static_cast<unsigned long long>(my_bad));
     __syncthreads();
     stamp(p, 2);
 
-    // local partial row -> s_part[rank]
+    // all CTAs of the cluster have started (they arrived at kernel entry) before
+    // anyone writes into a peer's shared memory
+    if (R > 1) cluster_wait();
     int32_t *row = s_part + rank * L.NP;
-    if (!PRIV) {
-        for (int e = warp; e < N; e += kWarps) {
-            int v = (lane < p.C) ? s_hist[e * p.C + lane] : 0;
-            v = __reduce_add_sync(kFull, v);
-            if (lane == 0) row[e] = v;
-        }
-    } else {
-        for (int e = tid; e < N; e += kThreads) {
-            int s = 0;
+    for (int e = tid; e < N; e += kThreads) {
+        int s = 0;
+        if (!PRIV) {
+            const int C = p.C;
+            if (C >= 4) {
+                // bank-rotated 128-bit loads: the 8 lanes of a quarter-warp phase hit
+                // 8 distinct 16-byte bank groups
+                const int q4 = C / 4;
+                const int4 *h4 = reinterpret_cast<const int4 *>(s_hist + e * C);
+                for (int q = 0; q < q4; ++q) {
+                    const int4 v = h4[(q + lane) & (q4 - 1)];
+                    s += v.x + v.y + v.z + v.w;
+                }
+            } else {
+                for (int c = 0; c < C; ++c) s += s_hist[e * C + c];
+            }
+        } else {
 #pragma unroll 4
             for (int w = 0; w < kWarps; ++w) s += s_hist[w * N + e];
-            row[e] = s;
         }
+        row[e] = s;
+        for (uint32_t d = 1; d < R; ++d) dsmem_st(row + e, (rank + d) % R, static_cast<uint32_t>(s));
     }
-    if (tid == 0) {
-        row[N] = misc[M_BAD_LO];
-        row[N + 1] = misc[M_BAD_HI];
+    if (tid < 2) {
+        const int32_t v = misc[M_BAD_LO + tid];
+        row[N + tid] = v;
+        for (uint32_t d = 1; d < R; ++d) dsmem_st(row + N + tid, (rank + d) % R, static_cast<uint32_t>(v));
     }
-    for (int e = N + 2 + tid; e < L.NP; e += kThreads) row[e] = 0;
-    __syncthreads();
-    // all CTAs of the cluster have started (arrived at kernel entry) before
-    // anyone writes into a peer's shared memory
-    cluster_wait();
-    const int nv = L.NP / 4;
-    for (int idx = tid; idx < (int)(R - 1) * nv; idx += kThreads) {
-        const uint32_t d = (rank + 1 + idx / nv) % R;
-        const int v = idx % nv;
-        const uint4 val = reinterpret_cast<const uint4 *>(row)[v];
-        dsmem_st_v4(reinterpret_cast<const uint4 *>(row) + v, d, val);
+    if (R > 1) {
+        cluster_arrive_release();
+        cluster_wait();
+    } else {
+        __syncthreads();
     }
-    cluster_arrive_release();
-    cluster_wait();
     stamp(p, 3);
+}
 
-    // reduce partials: T (all CTAs, redundantly); EPLB also keeps the CTA base
-    for (int e = tid; e < N; e += kThreads) {
-        uint32_t t = 0, b = 0;
-        for (uint32_t r = 0; r < R; ++r) {
-            const uint32_t v = static_cast<uint32_t>(s_part[r * L.NP + e]);
-            if (r < rank) b += v;
-            t += v;
-        }
-        s_T[e] = t;
-        if (BASE) s_T[N + e] = b;
+// cluster-wide min over the R rows' bad words; warp 0 only; publishes to misc
+__device__ __forceinline__ void bad_min_warp0(const Layout &L, unsigned char *smem, uint32_t R, int N) {
+    if ((threadIdx.x >> 5) != kWarps - 1) return;  // the last warp: idle in classify for N <= 480
+    int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
+    const int32_t *s_part = reinterpret_cast<const int32_t *>(smem + L.part);
+    const int lane = threadIdx.x & 31;
+    uint32_t lo = kBadLo, hi = kBadHi;
+    if (static_cast<uint32_t>(lane) < R) {
+        lo = static_cast<uint32_t>(s_part[lane * L.NP + N]);
+        hi = static_cast<uint32_t>(s_part[lane * L.NP + N + 1]);
     }
-    if (tid == 0) {
-        unsigned long long bad = static_cast<unsigned long long>(kNoBad);
-        for (uint32_t r = 0; r < R; ++r) {
-            const int32_t *rw = s_part + r * L.NP;
-            const unsigned long long v =
-                (static_cast<unsigned long long>(static_cast<uint32_t>(rw[N + 1])) << 32) |
-                static_cast<uint32_t>(rw[N]);
-            bad = min(bad, v);
-        }
-        misc[M_BADALL_LO] = static_cast<int32_t>(bad & 0xffffffffu);
-        misc[M_BADALL_HI] = static_cast<int32_t>(bad >> 32);
+    const bool bad = (lo != kBadLo) || (hi != kBadHi);
+    if (!__any_sync(kFull, bad)) return;  // common path: one vote
+    const uint32_t mhi = __reduce_min_sync(kFull, hi);
+    const uint32_t mlo = __reduce_min_sync(kFull, hi == mhi ? lo : 0xffffffffu);
+    if (lane == 0) {
+        misc[M_BADALL_LO] = static_cast<int32_t>(mlo);
+        misc[M_BADALL_HI] = static_cast<int32_t>(mhi);
     }
-    __syncthreads();
-    const unsigned long long bad =
-        (static_cast<unsigned long long>(static_cast<uint32_t>(misc[M_BADALL_HI])) << 32) |
-        static_cast<uint32_t>(misc[M_BADALL_LO]);
-    if (bad != static_cast<unsigned long long>(kNoBad)) {
-        if (rank == 0 && tid == 0) {
-            p.status[0] = METRO_ERR_ID_RANGE;
-            p.status[1] = static_cast<int32_t>(bad & 0xffffffffu);
-            p.status[2] = static_cast<int32_t>(bad >> 32);
-            p.status[3] = p.ids[bad];
-        }
-        return false;
+}
+
+// after a __syncthreads: report an out-of-range id (status by CTA 0) and bail
+__device__ __forceinline__ bool bad_after_sync(const Params &p, const Layout &L, unsigned char *smem,
+                                               uint32_t rank) {
+    const int32_t *misc = reinterpret_cast<const int32_t *>(smem + L.misc);
+    const uint32_t lo = static_cast<uint32_t>(misc[M_BADALL_LO]), hi = static_cast<uint32_t>(misc[M_BADALL_HI]);
+    if (lo == kBadLo && hi == kBadHi) return false;
+    if (rank == 0 && threadIdx.x == 0) {
+        const int64_t bad = join64(lo, hi);
+        p.status[0] = METRO_ERR_ID_RANGE;
+        p.status[1] = static_cast<int32_t>(lo);
+        p.status[2] = static_cast<int32_t>(hi);
+        p.status[3] = p.ids[bad];
     }
     return true;
 }
 
-__device__ void zero_smem(unsigned char *smem, int from, int to) {
-    for (int i = from / 16 + threadIdx.x; i < to / 16; i += kThreads)
-        reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0, 0, 0, 0);
+__device__ __forceinline__ void write_error(const Params &p, bool writer, int code, int32_t a) {
+    if (writer && threadIdx.x == 0) {
+        p.status[0] = code;
+        p.status[1] = a;
+        p.status[2] = 0;
+        p.status[3] = 0;
+    }
 }
 
-__device__ void init_misc(int32_t *misc) {
-    if (threadIdx.x < 64) misc[threadIdx.x] = 0;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        misc[M_BAD_LO] = static_cast<int32_t>(0xffffffffu);
-        misc[M_BAD_HI] = 0x7fffffff;
-        misc[M_NOREP] = INT32_MAX;
+// ---------------------------------------------------------------- phase D (METRO)
+// Packed single-thread greedy for G <= 8 ranks while every rank hosts at most
+// 126 active experts (so every L[g] <= 126 < 127): the 8 counters live as bytes
+// in two registers.  Measured on B200 (tools/latency_probe.cu): a compare that
+// produces a predicate costs 12-18 cycles on a dependent chain while PRMT / IADD
+// cost 3-4, so the chain is predicate-free:
+//   v_g   = PRMT(lo, sel_g, hi)       byte g zero-extended (sign-fill of a byte < 128)
+//   m     = sign(v_b - v_a)           all ones iff b wins strictly (PRMT sign replicate)
+//   L    += inc_a ^ ((inc_a ^ inc_b) & m)   (one LOP3 per half, then IADD)
+// Candidates arrive in ascending rank id, so "first minimum" (routing.py:96-98,
+// strict '<') means a later candidate wins only on strictly smaller L.
+struct PackedL {
+    uint32_t lo, hi;
+};
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t sel, uint32_t b) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+// zero-extended byte g of {lo, hi}: nibble0 = g, nibbles1..3 = sign-fill of byte g
+__host__ __device__ constexpr uint32_t zsel(uint32_t g) {
+    return g | ((8u | g) << 4) | ((8u | g) << 8) | ((8u | g) << 12);
+}
+__device__ __forceinline__ uint32_t sgn(uint32_t d) { return prmt(d, 0xBBBBu, 0u); }  // 0 or ~0
+__device__ __forceinline__ uint32_t pick(uint32_t a, uint32_t x, uint32_t m) {
+    uint32_t d;  // a ^ (x & m)
+    asm("lop3.b32 %0, %1, %2, %3, 0x78;" : "=r"(d) : "r"(a), "r"(x), "r"(m));
+    return d;
+}
+__device__ __forceinline__ uint4 lds4(const uint32_t *p) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(smem_u32(p)));
+    return v;
+}
+__host__ __device__ constexpr uint32_t inc_lo(uint32_t g) { return g < 4 ? (1u << (8 * g)) : 0u; }
+__host__ __device__ constexpr uint32_t inc_hi(uint32_t g) { return g >= 4 ? (1u << (8 * (g - 4))) : 0u; }
+
+// Entry layouts (words):
+//   r=2  {selA, selB, incA_lo, incA_hi, xAB_lo, xAB_hi, ga | gb << 8, id}
+//   r=3  {selA, selB, selC, 0, incA_lo, incA_hi, xAB_lo, xAB_hi, incC_lo, incC_hi,
+//         ga | gb << 8 | gc << 16, id}
+//   r>=4 {nc0..nc7 (127 for non-candidates, else 0), id, 0, 0, 0}
+__device__ __forceinline__ void packed_entry(uint32_t *dst, int r, uint32_t m, int e) {
+    if (r == 2 || r == 3) {
+        const uint32_t m1 = m & (m - 1), m2 = m1 & (m1 - 1);
+        const uint32_t g[3] = {static_cast<uint32_t>(__ffs(m) - 1), static_cast<uint32_t>(__ffs(m1) - 1),
+                               static_cast<uint32_t>(__ffs(m2) - 1)};
+        const uint32_t xlo = inc_lo(g[0]) ^ inc_lo(g[1]), xhi = inc_hi(g[0]) ^ inc_hi(g[1]);
+        if (r == 2) {
+            reinterpret_cast<uint4 *>(dst)[0] = make_uint4(zsel(g[0]), zsel(g[1]), inc_lo(g[0]), inc_hi(g[0]));
+            reinterpret_cast<uint4 *>(dst)[1] = make_uint4(xlo, xhi, g[0] | (g[1] << 8), static_cast<uint32_t>(e));
+        } else {
+            reinterpret_cast<uint4 *>(dst)[0] = make_uint4(zsel(g[0]), zsel(g[1]), zsel(g[2]), 0u);
+            reinterpret_cast<uint4 *>(dst)[1] = make_uint4(inc_lo(g[0]), inc_hi(g[0]), xlo, xhi);
+            reinterpret_cast<uint4 *>(dst)[2] =
+                make_uint4(inc_lo(g[2]), inc_hi(g[2]), g[0] | (g[1] << 8) | (g[2] << 16), static_cast<uint32_t>(e));
+        }
+    } else {
+        uint32_t nc[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) nc[g] = ((m >> g) & 1u) ? 0u : 127u;
+        reinterpret_cast<uint4 *>(dst)[0] = make_uint4(nc[0], nc[1], nc[2], nc[3]);
+        reinterpret_cast<uint4 *>(dst)[1] = make_uint4(nc[4], nc[5], nc[6], nc[7]);
+        reinterpret_cast<uint4 *>(dst)[2] = make_uint4(static_cast<uint32_t>(e), 0u, 0u, 0u);
     }
+}
+
+// one tournament node: right wins only on strictly smaller value
+struct Cand {
+    uint32_t v, ilo, ihi, g;
+};
+__device__ __forceinline__ Cand duel(const Cand &l, const Cand &r) {
+    const uint32_t m = sgn(r.v - l.v);
+    Cand o;
+    o.v = pick(l.v, l.v ^ r.v, m);
+    o.ilo = pick(l.ilo, l.ilo ^ r.ilo, m);
+    o.ihi = pick(l.ihi, l.ihi ^ r.ihi, m);
+    o.g = pick(l.g, l.g ^ r.g, m);
+    return o;
+}
+
+// One thread.  n2/n3/ng: step counts of each segment (sorted order is r asc, so
+// the segments are contiguous).  The r=2 array is padded to 4 plus one readable
+// group for the prefetch; the r=3 array to 2; padding entries are no-ops (zero
+// increments, choice into the dummy slot N).
+__device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t *e2, int n2, const uint32_t *e3,
+                                                 int n3, const uint32_t *eg, int ng, int32_t *s_choice, PackedL L) {
+    if (n2 > 0) {
+        uint4 a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            a[i] = lds4(e2 + i * kE2);
+            b[i] = lds4(e2 + i * kE2 + 4);
+        }
+        for (int s = 0; s < n2; s += 4) {
+            uint4 an[4], bn[4];
+            const uint32_t *nx = e2 + (s + 4) * kE2;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                an[i] = lds4(nx + i * kE2);
+                bn[i] = lds4(nx + i * kE2 + 4);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t va = prmt(L.lo, a[i].x, L.hi), vb = prmt(L.lo, a[i].y, L.hi);
+                const uint32_t m = sgn(vb - va);
+                L.lo += pick(a[i].z, b[i].x, m);
+                L.hi += pick(a[i].w, b[i].y, m);
+                const uint32_t gs = b[i].z;
+                s_choice[b[i].w] = static_cast<int32_t>(pick(gs & 0xffu, (gs ^ (gs >> 8)) & 0xffu, m));
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                a[i] = an[i];
+                b[i] = bn[i];
+            }
+        }
+    }
+    stamp(p, 8);
+    for (int s = 0; s < n3; s += 2) {
+        uint4 a[2], b[2], c[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            a[i] = lds4(e3 + (s + i) * kE3);
+            b[i] = lds4(e3 + (s + i) * kE3 + 4);
+            c[i] = lds4(e3 + (s + i) * kE3 + 8);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const uint32_t va = prmt(L.lo, a[i].x, L.hi), vb = prmt(L.lo, a[i].y, L.hi);
+            const uint32_t vc = prmt(L.lo, a[i].z, L.hi);
+            const uint32_t m1 = sgn(vb - va);
+            const uint32_t vab = pick(va, va ^ vb, m1);
+            const uint32_t ilo = pick(b[i].x, b[i].z, m1), ihi = pick(b[i].y, b[i].w, m1);
+            const uint32_t m2 = sgn(vc - vab);
+            L.lo += pick(ilo, ilo ^ c[i].x, m2);
+            L.hi += pick(ihi, ihi ^ c[i].y, m2);
+            const uint32_t gs = c[i].z, ga = gs & 0xffu, gb = (gs >> 8) & 0xffu, gc = (gs >> 16) & 0xffu;
+            const uint32_t gab = pick(ga, ga ^ gb, m1);
+            s_choice[c[i].w] = static_cast<int32_t>(pick(gab, gab ^ gc, m2));
+        }
+    }
+    stamp(p, 9);
+    for (int s = 0; s < ng; ++s) {
+        const uint4 n0 = lds4(eg + s * kE3), n1 = lds4(eg + s * kE3 + 4), n2v = lds4(eg + s * kE3 + 8);
+        const uint32_t nc[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+        Cand c[8];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            c[g].v = prmt(L.lo, zsel(g), L.hi) | nc[g];
+            c[g].ilo = inc_lo(g);
+            c[g].ihi = inc_hi(g);
+            c[g].g = g;
+        }
+        const Cand w = duel(duel(duel(c[0], c[1]), duel(c[2], c[3])), duel(duel(c[4], c[5]), duel(c[6], c[7])));
+        L.lo += w.ilo;
+        L.hi += w.ihi;
+        s_choice[n2v.x] = static_cast<int32_t>(w.g);
+    }
+    stamp(p, 10);
+    return L;
+}
+
+// Classify + sort + greedy.  MODE selects where T comes from: the cluster's
+// partial rows (kFromIds), the int64 loads argument (kFromLoads), or nowhere
+// (kFromOrder: a caller order, every listed expert goes through the greedy).
+// Returns false on error (status written by the writer CTA).
+template <int W, int MODE>
+__device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *smem, bool writer, uint32_t R,
+                             uint32_t rank) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int N = p.N, G = p.G;
+    int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
+    const uint32_t *s_mask = reinterpret_cast<const uint32_t *>(smem + L.mask);
+    uint32_t *s_T = reinterpret_cast<uint32_t *>(smem + L.T);
+    int32_t *s_choice = reinterpret_cast<int32_t *>(smem + L.choice);
+    const int32_t *s_part = reinterpret_cast<const int32_t *>(smem + L.part);
+    uint64_t *s_keys = reinterpret_cast<uint64_t *>(smem + L.keys);
+    int32_t *s_cand = reinterpret_cast<int32_t *>(smem + L.cand);
+    uint32_t *s_smask = reinterpret_cast<uint32_t *>(smem + L.smask);
+    int32_t *s_sid = reinterpret_cast<int32_t *>(smem + L.sid);
+    int32_t *s_L0 = reinterpret_cast<int32_t *>(smem + L.aux);
+    int32_t *s_hosted = s_L0 + kMaxG;  // active experts hosted per rank (bound on L[g])
+    uint32_t *s_ent = reinterpret_cast<uint32_t *>(smem + L.ent);
+
+    int m2 = 0, n2 = 0, n3 = 0;
+    bool packed = false;
+    if (MODE != kFromOrder) {
+        if (MODE == kFromIds) bad_min_warp0(L, smem, R, N);
+        for (int base = 0; base < N; base += kThreads) {
+            if (base + warp * 32 >= N) break;  // warp-uniform: no experts for this warp
+            const int e = base + tid;
+            const bool valid = e < N;
+            uint32_t t = 0;
+            if (valid) {
+                if (MODE == kFromIds) {
+#pragma unroll 4
+                    for (uint32_t r = 0; r < R; ++r) t += static_cast<uint32_t>(s_part[r * L.NP + e]);
+                } else {
+                    const int64_t tl = p.loads_in[e];
+                    if (tl < 0 || tl > 0xffffffffLL) misc[M_LOADERR] = 1;
+                    t = static_cast<uint32_t>(tl);
+                }
+                s_T[e] = t;
+            }
+            uint32_t mw[W];
+            int r = 0;
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                mw[j] = valid ? s_mask[e * W + j] : 0u;
+                r += __popc(mw[j]);
+            }
+            if (base == 0) stamp(p, 14);
+            const bool active = t > 0;
+            if (active && r == 0) atomicMin(&misc[M_NOREP], e);
+            const bool forced = active && r == 1;
+            const bool multi = active && r >= 2;
+            int g1 = -1;
+            if (forced) {
+#pragma unroll
+                for (int j = W - 1; j >= 0; --j)
+                    if (mw[j]) g1 = 32 * j + __ffs(mw[j]) - 1;
+            }
+            if (valid) s_choice[e] = g1;
+            if (base == 0) stamp(p, 15);
+            // forced prefix: per-rank counts of single-replica active experts.  Their
+            // order is irrelevant: each lands on its only replica.
+            // Also count active experts hosted per rank: max <= 255 admits the packed greedy.
+            if (W == 1) {
+                int cnt = 0, host = 0;
+                for (int g = 0; g < G; ++g) {
+                    const unsigned b = __ballot_sync(kFull, g1 == g);
+                    const unsigned h = __ballot_sync(kFull, active && ((mw[0] >> g) & 1u));
+                    if (lane == g) {
+                        cnt = __popc(b);
+                        host = __popc(h);
+                    }
+                }
+                if (lane < G) {
+                    if (cnt) atomicAdd(&s_L0[lane], cnt);
+                    if (host) atomicAdd(&s_hosted[lane], host);
+                }
+            } else if (forced) {
+                atomicAdd(&s_L0[g1], 1);
+            }
+            // compact replicated active experts (any order: the sort ranks them)
+            if (base == 0) stamp(p, 16);
+            const unsigned bm = __ballot_sync(kFull, multi);
+            int seg = 0;
+            if (lane == 0 && bm) seg = atomicAdd(&misc[M_M2], __popc(bm));
+            const unsigned b2 = __ballot_sync(kFull, multi && r == 2);
+            const unsigned b3 = __ballot_sync(kFull, multi && r == 3);
+            if (lane == 0) {
+                if (b2) atomicAdd(&misc[M_N2], __popc(b2));
+                if (b3) atomicAdd(&misc[M_N3], __popc(b3));
+            }
+            seg = __shfl_sync(kFull, seg, 0);
+            if (base == 0) stamp(p, 17);
+            if (multi) {
+                const int off = seg + __popc(bm & lanemask_lt());
+                // canonical key (routing.py:84-86): r asc, T desc, id asc
+                s_keys[off] = (static_cast<uint64_t>(r) << 56) | (static_cast<uint64_t>(0xffffffffu - t) << 24) |
+                              static_cast<uint64_t>(e);
+                s_cand[off] = e;
+            }
+        }
+        stamp(p, 11);
+        __syncthreads();
+        stamp(p, 12);
+        if (MODE == kFromIds && bad_after_sync(p, L, smem, rank)) return false;
+        if (MODE == kFromLoads && misc[M_LOADERR]) {
+            write_error(p, writer, METRO_ERR_LOAD_RANGE, 0);
+            return false;
+        }
+        if (misc[M_NOREP] != INT32_MAX) {
+            write_error(p, writer, METRO_ERR_NO_REPLICA, misc[M_NOREP]);
+            return false;
+        }
+        m2 = misc[M_M2];
+        n2 = misc[M_N2];
+        n3 = misc[M_N3];
+        if (W == 1 && G <= 8) {
+            int mx = 0;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) mx = max(mx, g < G ? s_hosted[g] : 0);
+            packed = mx <= 126;
+        }
+        if (tid < 8) s_keys[m2 + tid] = ~0ull;  // pad for the pairwise scan
+        __syncthreads();
+        stamp(p, 4);
+        // ---- rank-by-count sort: one thread per replicated expert, broadcast key reads
+        uint32_t *e2 = s_ent;
+        uint32_t *e3 = e2 + (align_up(n2, 4) + 4) * kE2;
+        uint32_t *eg = e3 + align_up(n3, 2) * kE3;
+        // four threads per candidate: each scans every 4th key pair, quad shuffle-sum
+        for (int c0 = 0; c0 < m2; c0 += kThreads / 4) {
+            const int c = c0 + (tid >> 2), part = tid & 3;
+            const uint64_t kc = (c < m2) ? s_keys[c] : 0ull;
+            int rk = 0;
+#pragma unroll 4
+            for (int c2 = 2 * part; c2 < m2; c2 += 8) {
+                const ulonglong2 kk = *reinterpret_cast<const ulonglong2 *>(s_keys + c2);
+                rk += (kk.x < kc) + (kk.y < kc);
+            }
+            rk += __shfl_xor_sync(kFull, rk, 1);
+            rk += __shfl_xor_sync(kFull, rk, 2);
+            if (c >= m2 || part != 0) continue;
+            if (c == 0) stamp(p, 13);
+            const int e = s_cand[c];
+            if (packed) {
+                const int r = static_cast<int>(kc >> 56);
+                if (rk < n2) packed_entry(e2 + rk * kE2, 2, s_mask[e], e);
+                else if (rk < n2 + n3) packed_entry(e3 + (rk - n2) * kE3, 3, s_mask[e], e);
+                else packed_entry(eg + (rk - n2 - n3) * kEG, r, s_mask[e], e);
+            } else {
+#pragma unroll
+                for (int j = 0; j < W; ++j) s_smask[j * N + rk] = s_mask[e * W + j];
+                s_sid[rk] = e;
+            }
+        }
+        if (packed && tid < 8) {  // no-op padding (zero increments, dummy choice slot N)
+            uint32_t *z2 = e2 + (n2 + tid) * kE2;
+            if (n2 + tid < align_up(n2, 4) + 4)
+                for (int w = 0; w < kE2; ++w) z2[w] = (w == 7) ? static_cast<uint32_t>(N) : 0u;
+            uint32_t *z3 = e3 + (n3 + tid) * kE3;
+            if (tid < 4 && n3 + tid < align_up(n3, 2))
+                for (int w = 0; w < kE3; ++w) z3[w] = (w == 11) ? static_cast<uint32_t>(N) : 0u;
+        }
+    } else {
+        // caller-supplied order (metro-parallel): single-replica experts included
+        m2 = p.order_len;
+        for (int s = tid; s < m2; s += kThreads) {
+            const int e = p.order[s];
+            int r = 0;
+            if (e >= 0 && e < N) {
+#pragma unroll
+                for (int j = 0; j < W; ++j) {
+                    const uint32_t w = s_mask[e * W + j];
+                    s_smask[j * N + s] = w;
+                    r += __popc(w);
+                }
+                s_sid[s] = e;
+            }
+            if (e < 0 || e >= N || r == 0) atomicMin(&misc[M_NOREP], (e < 0 || e >= N) ? -1 : e);
+        }
+        for (int e = tid; e < N; e += kThreads) s_choice[e] = -1;
+        __syncthreads();
+        if (misc[M_NOREP] != INT32_MAX) {
+            write_error(p, writer, METRO_ERR_NO_REPLICA, misc[M_NOREP]);
+            return false;
+        }
+    }
+    __syncthreads();
+    stamp(p, 5);
+
+    if (W == 1 && packed) {
+        if (tid == 0) {
+            PackedL Lp;
+            Lp.lo = Lp.hi = 0;
+            for (int g = 0; g < G; ++g) {
+                const uint32_t v = static_cast<uint32_t>(s_L0[g]) << (8 * (g & 3));
+                if (g < 4) Lp.lo += v;
+                else Lp.hi += v;
+            }
+            uint32_t *e2 = s_ent;
+            uint32_t *e3 = e2 + (align_up(n2, 4) + 4) * kE2;
+            uint32_t *eg = e3 + align_up(n3, 2) * kE3;
+            Lp = packed_greedy(p, e2, n2, e3, n3, eg, m2 - n2 - n3, s_choice, Lp);
+            s_L0[0] = static_cast<int32_t>(Lp.lo);
+            s_L0[1] = static_cast<int32_t>(Lp.hi);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t word = static_cast<uint32_t>(s_L0[lane >= 4 ? 1 : 0]);
+            const uint32_t c = lane < G ? ((word >> (8 * (lane & 3))) & 0xffu) : 0u;
+            if (writer && lane < G) p.rank_counts[lane] = static_cast<int32_t>(c);
+            const uint32_t mx = __reduce_max_sync(kFull, c);
+            if (writer && lane == 0) *p.lam = static_cast<int32_t>(mx);
+        }
+        stamp(p, 6);
+        return true;
+    }
+
+    // ---- serial greedy (routing.py:94-101) in warp 0, any G <= 128.
+    // Lane owns ranks g = lane + 32 k as packed keys (L << 8 | g): the warp-wide
+    // min over candidate lanes is "smallest L, then smallest g" -- the
+    // reference's ascending scan with strict '<'.  Per chunk of 32 steps the
+    // candidacy bits are transposed with ballots (lane g gets bit s of step s),
+    // so the chain SEL -> redux.min -> ISETP -> IADD touches no memory.
+    if (warp == 0) {
+        uint32_t Lk[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const int g = lane + 32 * k;
+            Lk[k] = (g < G) ? ((static_cast<uint32_t>(s_L0[g]) << 8) | static_cast<uint32_t>(g)) : 0xffffffffu;
+        }
+        for (int base = 0; base < m2; base += 32) {
+            const int j = base + lane;
+            const bool v = j < m2;
+            uint32_t cb[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const uint32_t m = v ? s_smask[k * N + j] : 0u;
+                cb[k] = 0;
+                const int gk = min(32, G - 32 * k);
+                for (int b = 0; b < gk; ++b) {
+                    const unsigned bb = __ballot_sync(kFull, (m >> b) & 1u);
+                    if (lane == b) cb[k] = bb;
+                }
+            }
+            const int myid = v ? s_sid[j] : 0;
+            const int steps = min(32, m2 - base);
+            uint32_t wmine = 0;
+#pragma unroll
+            for (int s = 0; s < 32; ++s) {
+                if (s >= steps) break;
+                uint32_t val = 0xffffffffu;
+#pragma unroll
+                for (int k = 0; k < W; ++k) val = ((cb[k] >> s) & 1u) ? min(val, Lk[k]) : val;
+                const uint32_t win = __reduce_min_sync(kFull, val);
+#pragma unroll
+                for (int k = 0; k < W; ++k) Lk[k] += (Lk[k] == win) ? 256u : 0u;
+                wmine = (lane == s) ? win : wmine;
+            }
+            if (v) s_choice[myid] = static_cast<int32_t>(wmine & 0xffu);
+        }
+        uint32_t mx = 0;
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const int g = lane + 32 * k;
+            if (g < G) {
+                const uint32_t c = Lk[k] >> 8;
+                if (writer) p.rank_counts[g] = static_cast<int32_t>(c);
+                mx = max(mx, c);
+            }
+        }
+        mx = __reduce_max_sync(kFull, mx);
+        if (writer && lane == 0) *p.lam = static_cast<int32_t>(mx);
+    }
+    __syncthreads();
+    stamp(p, 6);
+    return true;
 }
 
 // ================================================================ kernels
 template <int W>
 __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
-    cluster_arrive_relaxed();  // paired with the wait before the first DSMEM store
-    stamp(p, 0);
     const uint32_t R = cluster_nctarank(), rank = cluster_ctarank();
+    if (R > 1) cluster_arrive_relaxed();  // paired with the wait before the first DSMEM store
     const Layout L = make_layout(kMetroIds, p.N, W, R, p.slice, p.C, p.staged);
-    int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
     const int64_t beg = static_cast<int64_t>(rank) * p.slice;
     const int64_t rem_pairs = p.num_pairs - beg;
     const int n_local = rem_pairs <= 0 ? 0 : static_cast<int>(rem_pairs < p.slice ? rem_pairs : p.slice);
-
+    const StagePlan sp = stage_plan<W>(p, beg, n_local, p.staged != 0);
+    if (threadIdx.x == 0) stage_issue(p, L, smem, beg, sp);
+    stamp(p, 0);
+    int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
     init_misc(misc);
     zero_smem(smem, L.aux, L.part);  // forced counts + histogram
-    stage_inputs<W>(p, L, smem, beg, n_local, p.staged != 0);
+    stage_rest(p, L, smem, beg, n_local, p.staged != 0, sp);
+    __syncthreads();
+    mbar_wait(reinterpret_cast<uint64_t *>(smem + L.mbar), 0);
     stamp(p, 1);
-    if (!histogram_exchange<W, false, false>(p, L, smem, beg, n_local, R, rank)) return;
+    histogram_push<false>(p, L, smem, beg, n_local, R, rank);
     const bool writer = (rank == 0);
     if (!p.mask) {  // aggregate_loads only (core.py:236-244)
+        bad_min_warp0(L, smem, R, p.N);
+        __syncthreads();
+        if (bad_after_sync(p, L, smem, rank)) return;
         if (writer) {
-            const uint32_t *s_T = reinterpret_cast<const uint32_t *>(smem + L.T);
-            for (int e = threadIdx.x; e < p.N; e += kThreads) p.loads[e] = static_cast<int32_t>(s_T[e]);
+            const int32_t *s_part = reinterpret_cast<const int32_t *>(smem + L.part);
+            for (int e = threadIdx.x; e < p.N; e += kThreads) {
+                int32_t t = 0;
+                for (uint32_t r = 0; r < R; ++r) t += s_part[r * L.NP + e];
+                p.loads[e] = t;
+            }
             if (threadIdx.x == 0) {
                 p.status[0] = METRO_OK;
                 p.status[1] = p.status[2] = 0;
@@ -592,7 +907,7 @@ __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) 
         }
         return;
     }
-    if (!metro_decide<W>(p, L, smem, writer, false)) return;
+    if (!metro_decide<W, kFromIds>(p, L, smem, writer, R, rank)) return;
 
     // ---- outputs
     const int32_t *s_choice = reinterpret_cast<const int32_t *>(smem + L.choice);
@@ -635,27 +950,16 @@ template <int W>
 __global__ void __launch_bounds__(kThreads, 1) metro_loads_kernel(const Params p, int ordered) {
     extern __shared__ __align__(128) unsigned char smem[];
     const Layout L = make_layout(ordered ? kMetroOrdered : kMetroLoads, p.N, W, 1, 0, 1, 0);
-    int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
-    uint32_t *s_T = reinterpret_cast<uint32_t *>(smem + L.T);
-    init_misc(misc);
+    const StagePlan sp = stage_plan<W>(p, 0, 0, false);
+    if (threadIdx.x == 0) stage_issue(p, L, smem, 0, sp);
+    init_misc(reinterpret_cast<int32_t *>(smem + L.misc));
     zero_smem(smem, L.aux, L.hist);
-    stage_inputs<W>(p, L, smem, 0, 0, false);
-    if (!ordered) {
-        for (int e = threadIdx.x; e < p.N; e += kThreads) {
-            const int64_t t = p.loads_in[e];
-            if (t < 0 || t > 0xffffffffLL) atomicMax(&misc[M_LOADERR], 1);
-            s_T[e] = static_cast<uint32_t>(t);
-        }
-        __syncthreads();
-        if (misc[M_LOADERR]) {
-            if (threadIdx.x == 0) {
-                p.status[0] = METRO_ERR_LOAD_RANGE;
-                p.status[1] = p.status[2] = p.status[3] = 0;
-            }
-            return;
-        }
-    }
-    if (!metro_decide<W>(p, L, smem, true, ordered != 0)) return;
+    stage_rest(p, L, smem, 0, 0, false, sp);
+    __syncthreads();
+    mbar_wait(reinterpret_cast<uint64_t *>(smem + L.mbar), 0);
+    const bool ok = ordered ? metro_decide<W, kFromOrder>(p, L, smem, true, 1, 0)
+                            : metro_decide<W, kFromLoads>(p, L, smem, true, 1, 0);
+    if (!ok) return;
     const int32_t *s_choice = reinterpret_cast<const int32_t *>(smem + L.choice);
     for (int e = threadIdx.x; e < p.N; e += kThreads) p.choice[e] = s_choice[e];
     if (threadIdx.x == 0) {
@@ -666,11 +970,11 @@ __global__ void __launch_bounds__(kThreads, 1) metro_loads_kernel(const Params p
 }
 
 // ---------------------------------------------------------------- EPLB
-// Shared by both EPLB kernels: per-rank activated counts (y = x > 0), lam, x.
-// T64 supplies the load of expert e.
+// Per-rank activated counts (y = x > 0 on the first min(T, r) replicas), lam, x.
+// T64 supplies the load of expert e.  Returns false on a missing replica.
 template <int W, typename LoadFn, typename XT>
-__device__ void eplb_counts_and_x(const Params &p, const Layout &L, unsigned char *smem,
-                                  bool writer, LoadFn T64, XT *x) {
+__device__ bool eplb_counts_and_x(const Params &p, const Layout &L, unsigned char *smem, bool writer, LoadFn T64,
+                                  XT *x) {
     const int tid = threadIdx.x, lane = tid & 31;
     const int N = p.N, G = p.G;
     const uint32_t *s_mask = reinterpret_cast<const uint32_t *>(smem + L.mask);
@@ -692,15 +996,18 @@ __device__ void eplb_counts_and_x(const Params &p, const Layout &L, unsigned cha
         int64_t a = (t < r) ? t : r;
 #pragma unroll
         for (int j = 0; j < W; ++j) {
-            const int c = __popc(mw[j]);
-            const int take = static_cast<int>(a < c ? a : c);
-            act[j] = (take == c) ? mw[j] : (take == 0 ? 0u : (mw[j] & ((1u << __fns(mw[j], 0, take + 1)) - 1u)));
-            a -= take;
+            uint32_t m = mw[j], keep = 0;
+            while (a > 0 && m) {
+                const uint32_t low = m & (0u - m);
+                keep |= low;
+                m ^= low;
+                --a;
+            }
+            act[j] = keep;
         }
         if (W == 1) {
-            // per-rank column sums with one ballot per rank
-            int mine = 0;
-            for (int g = 0; g < G && g < 32; ++g) {
+            int mine = 0;  // per-rank column sums with one ballot per rank
+            for (int g = 0; g < G; ++g) {
                 const unsigned b = __ballot_sync(kFull, (act[0] >> g) & 1u);
                 if (lane == g) mine = __popc(b);
             }
@@ -718,7 +1025,10 @@ __device__ void eplb_counts_and_x(const Params &p, const Layout &L, unsigned cha
         }
     }
     __syncthreads();
-    if (misc[M_NOREP] != INT32_MAX) return;
+    if (misc[M_NOREP] != INT32_MAX) {
+        write_error(p, writer, METRO_ERR_NO_REPLICA, misc[M_NOREP]);
+        return false;
+    }
     if (writer) {
         if (tid < 32) {
             int mx = 0;
@@ -752,40 +1062,53 @@ __device__ void eplb_counts_and_x(const Params &p, const Layout &L, unsigned cha
             }
         }
     }
+    return true;
 }
 
 template <int W, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) eplb_ids_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
-    cluster_arrive_relaxed();
     const uint32_t R = cluster_nctarank(), rank = cluster_ctarank();
+    if (R > 1) cluster_arrive_relaxed();
     const Layout L = make_layout(kEplbIds, p.N, W, R, p.slice, p.C, p.staged, PAIR);
-    int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
     const int64_t beg = static_cast<int64_t>(rank) * p.slice;
     const int64_t rem_pairs = p.num_pairs - beg;
     const int n_local = rem_pairs <= 0 ? 0 : static_cast<int>(rem_pairs < p.slice ? rem_pairs : p.slice);
+    const StagePlan sp = stage_plan<W>(p, beg, n_local, p.staged != 0);
+    if (threadIdx.x == 0) stage_issue(p, L, smem, beg, sp);
+    int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
     init_misc(misc);
     zero_smem(smem, L.aux, L.part);  // rank counts + histogram
-    stage_inputs<W>(p, L, smem, beg, n_local, p.staged != 0);
-    if (!histogram_exchange<W, PAIR, true>(p, L, smem, beg, n_local, R, rank)) return;
+    stage_rest(p, L, smem, beg, n_local, p.staged != 0, sp);
+    __syncthreads();
+    mbar_wait(reinterpret_cast<uint64_t *>(smem + L.mbar), 0);
+    histogram_push<PAIR>(p, L, smem, beg, n_local, R, rank);
     const bool writer = (rank == 0);
-    const uint32_t *s_T = reinterpret_cast<const uint32_t *>(smem + L.T);
-    eplb_counts_and_x<W>(p, L, smem, writer, [&](int e) { return static_cast<int64_t>(s_T[e]); }, p.x32);
-    if (misc[M_NOREP] != INT32_MAX) {
-        if (writer && threadIdx.x == 0) {
-            p.status[0] = METRO_ERR_NO_REPLICA;
-            p.status[1] = misc[M_NOREP];
-            p.status[2] = p.status[3] = 0;
+    const int N = p.N;
+    uint32_t *s_T = reinterpret_cast<uint32_t *>(smem + L.T);
+    const int32_t *s_part = reinterpret_cast<const int32_t *>(smem + L.part);
+    bad_min_warp0(L, smem, R, N);
+    for (int e = threadIdx.x; e < N; e += kThreads) {
+        uint32_t t = 0, b = 0;
+        for (uint32_t r = 0; r < R; ++r) {
+            const uint32_t v = static_cast<uint32_t>(s_part[r * L.NP + e]);
+            b += (r < rank) ? v : 0u;
+            t += v;
         }
-        return;
+        s_T[e] = t;
+        s_T[N + e] = b;  // occurrences of e in earlier CTAs' slices
     }
+    __syncthreads();
+    if (bad_after_sync(p, L, smem, rank)) return;
+    if (!eplb_counts_and_x<W>(p, L, smem, writer, [&](int e) { return static_cast<int64_t>(s_T[e]); }, p.x32))
+        return;
     if (PAIR && p.pair_rank) {
         // occurrence o of expert e (global row-major) -> replica (o mod r_e)
-        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, N = p.N;
+        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
         int32_t *s_hist = reinterpret_cast<int32_t *>(smem + L.hist);
         const uint32_t *s_mask = reinterpret_cast<const uint32_t *>(smem + L.mask);
         for (int e = tid; e < N; e += kThreads) {
-            int run = static_cast<int>(s_T[N + e]);  // earlier CTAs
+            int run = static_cast<int>(s_T[N + e]);
             for (int w = 0; w < kWarps; ++w) {
                 const int c = s_hist[w * N + e];
                 s_hist[w * N + e] = run;
@@ -819,7 +1142,7 @@ __global__ void __launch_bounds__(kThreads, 1) eplb_ids_kernel(const Params p) {
         }
     }
     if (writer) {
-        for (int e = threadIdx.x; e < p.N; e += kThreads)
+        for (int e = threadIdx.x; e < N; e += kThreads)
             if (p.loads) p.loads[e] = static_cast<int32_t>(s_T[e]);
         if (threadIdx.x == 0) {
             p.status[0] = METRO_OK;
@@ -833,20 +1156,17 @@ template <int W>
 __global__ void __launch_bounds__(kThreads, 1) eplb_loads_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const Layout L = make_layout(kEplbLoads, p.N, W, 1, 0, 1, 0);
-    int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
-    init_misc(misc);
+    const StagePlan sp = stage_plan<W>(p, 0, 0, false);
+    if (threadIdx.x == 0) stage_issue(p, L, smem, 0, sp);
+    init_misc(reinterpret_cast<int32_t *>(smem + L.misc));
     zero_smem(smem, L.aux, L.hist);
-    stage_inputs<W>(p, L, smem, 0, 0, false);
-    eplb_counts_and_x<W>(p, L, smem, true, [&](int e) { return p.loads_in[e]; }, p.x64);
+    stage_rest(p, L, smem, 0, 0, false, sp);
+    __syncthreads();
+    mbar_wait(reinterpret_cast<uint64_t *>(smem + L.mbar), 0);
+    if (!eplb_counts_and_x<W>(p, L, smem, true, [&](int e) { return p.loads_in[e]; }, p.x64)) return;
     if (threadIdx.x == 0) {
-        if (misc[M_NOREP] != INT32_MAX) {
-            p.status[0] = METRO_ERR_NO_REPLICA;
-            p.status[1] = misc[M_NOREP];
-        } else {
-            p.status[0] = METRO_OK;
-            p.status[1] = 0;
-        }
-        p.status[2] = 0;
+        p.status[0] = METRO_OK;
+        p.status[1] = p.status[2] = 0;
         p.status[3] = 1;
     }
 }
@@ -907,7 +1227,11 @@ static int launch(K kernel, int R, int smem, cudaStream_t s, Args... args) {
 
 static int words_for(int G) { return (G + 31) / 32; }
 static int copies_for(int N) {
-    int C = 32;
+    static const int forced = [] {  // tuning override (power of two 1..32)
+        const char *v = getenv("METRO_HIST_COPIES");
+        return v ? atoi(v) : 0;
+    }();
+    int C = (forced >= 1 && forced <= 32 && (forced & (forced - 1)) == 0) ? forced : 32;
     while (C > 1 && N * C * 4 > 64 * 1024) C >>= 1;
     return C;
 }

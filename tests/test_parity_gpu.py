@@ -177,7 +177,10 @@ def test_max_sizes():
     A = (rng.random((n, g)) < 0.02).astype(np.int8)
     A[np.flatnonzero(A.sum(1) == 0), 0] = 1
     ids = rng.integers(0, n, size=(4096, 8)).astype(np.int32)
-    check_metro(ids, A, 16)
+    check_metro(ids, A, 0)  # auto plan shrinks the cluster until the layout fits
+    check_metro(ids, A, 2)
+    with pytest.raises(pkg.ValidationError, match="shared memory"):
+        metro_dev(ids, A, 16)  # 16 partial rows of 4096 experts cannot fit 227 KB
     ids = gen_zipf_topk(256, 8, 32768, 1.2, 3)  # 262144 pairs
     check_metro(ids, make_placement(256, 8, 1.5, 7).matrix, 16)
 
