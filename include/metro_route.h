@@ -138,16 +138,21 @@ METRO_API int eplb_route_from_loads_v1(const int64_t *loads, const uint32_t *ran
                              int32_t *rank_counts, int32_t *lam, int32_t *status,
                              void *stream);
 
-/* End-to-end METRO from HOST buffers: H2D of ids (pinned host memory gives the
- * async fast path), metro_route_v1, D2H of the results, stream synchronise.
- * dev_workspace must hold metro_host_workspace_bytes() bytes (256-aligned).
+/* End-to-end METRO from HOST buffers, synchronous.  Two transfer modes:
+ *   flags = 0                    : cudaMemcpyAsync H2D of the ids into dev_workspace
+ *                                  (metro_host_workspace_bytes() bytes), the kernel,
+ *                                  D2H of the results, stream synchronise;
+ *   flags = METRO_HOST_ZEROCOPY  : the kernel reads the ids from and writes the
+ *                                  results to pinned (device-mapped) host memory
+ *                                  directly over PCIe; dev_workspace unused.
  * host_out [8 + G + N] int32 receives: status[4], lam, pad[3], rank_counts[G],
  * choice[N].  pair_rank_host [num_pairs] is nullable. */
+#define METRO_HOST_ZEROCOPY 1
 METRO_API size_t metro_host_workspace_bytes(int64_t num_pairs, int32_t num_experts, int32_t num_ranks);
 METRO_API int metro_route_host_v1(const int32_t *topk_ids_host, int64_t num_pairs,
-                        const uint32_t *rank_mask_dev, int32_t num_experts, int32_t num_ranks,
-                        void *dev_workspace, int32_t *host_out, int32_t *pair_rank_host,
-                        int32_t cluster_ctas, void *stream);
+                                  const uint32_t *rank_mask_dev, int32_t num_experts, int32_t num_ranks,
+                                  void *dev_workspace, int32_t *host_out, int32_t *pair_rank_host,
+                                  int32_t cluster_ctas, int32_t flags, void *stream);
 
 /* Debug / tuning: per-phase clock64 stamps of CTA 0 of the next metro_route_v1
  * launch in this process are written to `stamps` (device, >= 16 int64) when set;

@@ -27,6 +27,7 @@ EARG = -1
 EDIMS = -2
 ECUDA = -3
 ENOTBINARY = -4
+HOST_ZEROCOPY = 1
 
 MAX_G = 128
 MAX_N = 4096
@@ -71,7 +72,7 @@ def lib() -> ctypes.CDLL:
         "eplb_route_v1": ([P, i64, P, i32, i32, P, P, P, P, P, P, i32, P], ctypes.c_int),
         "eplb_route_from_loads_v1": ([P, P, i32, i32, P, P, P, P, P], ctypes.c_int),
         "metro_host_workspace_bytes": ([i64, i32, i32], ctypes.c_size_t),
-        "metro_route_host_v1": ([P, i64, P, i32, i32, P, P, P, i32, P], ctypes.c_int),
+        "metro_route_host_v1": ([P, i64, P, i32, i32, P, P, P, i32, i32, P], ctypes.c_int),
         "metro_debug_set_stamps": ([P], None),
     }
     for name, (argtypes, restype) in sig.items():
@@ -84,14 +85,18 @@ def lib() -> ctypes.CDLL:
     return L
 
 
+HEADERS = ("metro_route.h", "moe_gemm.h")
+
+
 def exported_symbols() -> list:
-    """Names declared in include/metro_route.h (used by the ABI test)."""
-    hdr = os.path.join(os.path.dirname(_HERE), "include", "metro_route.h")
+    """Names declared in include/*.h (used by the ABI test)."""
     import re
 
-    with open(hdr) as f:
-        text = f.read()
-    return sorted(set(re.findall(r"METRO_API\s+[\w\s\*]+?\b(\w+)\s*\(", text)))
+    names = set()
+    for h in HEADERS:
+        with open(os.path.join(os.path.dirname(_HERE), "include", h)) as f:
+            names.update(re.findall(r"METRO_API\s+[\w\s\*]+?\b(\w+)\s*\(", f.read()))
+    return sorted(names)
 
 
 def check_rc(rc: int, what: str) -> None:

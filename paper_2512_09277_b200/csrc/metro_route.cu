@@ -85,7 +85,7 @@ struct Layout {
 __host__ __device__ inline int align_up(int x, int a) { return (x + a - 1) / a * a; }
 
 // packed greedy entry sizes (words): r = 2 / r = 3 / generic
-constexpr int kE2 = 8, kE3 = 12, kEG = 12;
+constexpr int kES = 12;  // packed greedy entry stride (words)
 
 __host__ __device__ inline Layout make_layout(int kind, int N, int W, int R, int64_t slice,
                                               int C, int staged, bool warp_hist = false) {
@@ -109,12 +109,12 @@ __host__ __device__ inline Layout make_layout(int kind, int N, int W, int R, int
     L.part = align_up(o + hist_bytes, 16);
     const int end1 = ids_mode ? align_up(L.part + R * L.NP * 4, 16) : L.part;
     L.keys = o;
-    L.cand = align_up(L.keys + (N + 8) * 8, 16);
+    L.cand = align_up(L.keys + (N + 16) * 8, 16);
     L.smask = align_up(L.cand + N * 4, 16);
     L.sid = align_up(L.smask + N * W * 4, 16);
     L.ent = align_up(L.sid + N * 4, 16);
-    // packed-greedy entries (W == 1 only): r=2, r=3 and generic arrays, padded by 4
-    const int end2 = metro ? align_up(L.ent + (W == 1 ? (N + 16) * kE3 * 4 : 0), 16) : o;
+    // packed-greedy entries (W == 1 only), one slot per rank + readable padding
+    const int end2 = metro ? align_up(L.ent + (W == 1 ? (N + 16) * kES * 4 : 0), 16) : o;
     L.total = end1 > end2 ? end1 : end2;
     return L;
 }
@@ -126,7 +126,8 @@ enum {
     M_LOADERR = 3,
     M_BADALL_LO = 4, M_BADALL_HI = 5,  // cluster-wide min bad pair index
     M_M2 = 6,                          // replicated active experts (compaction cursor)
-    M_N2 = 7, M_N3 = 8,                // of which r == 2 / r == 3
+    M_N2 = 7, M_N3 = 8,                // end of the r == 2 / r <= 3 segments (sorted order)
+    M_PACKED_LO = 9, M_PACKED_HI = 10, M_PACKED_OK = 11,
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -503,36 +504,38 @@ __device__ __forceinline__ Cand duel(const Cand &l, const Cand &r) {
     return o;
 }
 
-// One thread.  n2/n3/ng: step counts of each segment (sorted order is r asc, so
-// the segments are contiguous).  The r=2 array is padded to 4 plus one readable
-// group for the prefetch; the r=3 array to 2; padding entries are no-ops (zero
-// increments, choice into the dummy slot N).
-__device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t *e2, int n2, const uint32_t *e3,
-                                                 int n3, const uint32_t *eg, int ng, int32_t *s_choice, PackedL L) {
-    if (n2 > 0) {
+// One thread.  Entries live at slot = rank (stride kES words) and are grouped
+// by r because the canonical order sorts by r first: [0, n2) r=2,
+// [n2, n2 + n3) r=3, [n2 + n3, m2) r>=4.  Slots up to m2 + 8 are readable (the
+// r=2 prefetch may touch them; they are never applied).
+__device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t *ent, int n2, int n3, int m2,
+                                                 int32_t *s_choice, PackedL L) {
+    auto step2 = [&](const uint4 &a, const uint4 &b) {
+        const uint32_t va = prmt(L.lo, a.x, L.hi), vb = prmt(L.lo, a.y, L.hi);
+        const uint32_t m = sgn(vb - va);
+        L.lo += pick(a.z, b.x, m);
+        L.hi += pick(a.w, b.y, m);
+        const uint32_t gs = b.z;
+        s_choice[b.w] = static_cast<int32_t>(pick(gs & 0xffu, (gs ^ (gs >> 8)) & 0xffu, m));
+    };
+    int s = 0;
+    if (n2 >= 4) {
         uint4 a[4], b[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            a[i] = lds4(e2 + i * kE2);
-            b[i] = lds4(e2 + i * kE2 + 4);
+            a[i] = lds4(ent + i * kES);
+            b[i] = lds4(ent + i * kES + 4);
         }
-        for (int s = 0; s < n2; s += 4) {
+        for (; s + 4 <= n2; s += 4) {
             uint4 an[4], bn[4];
-            const uint32_t *nx = e2 + (s + 4) * kE2;
+            const uint32_t *nx = ent + (s + 4) * kES;  // readable even past n2
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                an[i] = lds4(nx + i * kE2);
-                bn[i] = lds4(nx + i * kE2 + 4);
+                an[i] = lds4(nx + i * kES);
+                bn[i] = lds4(nx + i * kES + 4);
             }
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const uint32_t va = prmt(L.lo, a[i].x, L.hi), vb = prmt(L.lo, a[i].y, L.hi);
-                const uint32_t m = sgn(vb - va);
-                L.lo += pick(a[i].z, b[i].x, m);
-                L.hi += pick(a[i].w, b[i].y, m);
-                const uint32_t gs = b[i].z;
-                s_choice[b[i].w] = static_cast<int32_t>(pick(gs & 0xffu, (gs ^ (gs >> 8)) & 0xffu, m));
-            }
+            for (int i = 0; i < 4; ++i) step2(a[i], b[i]);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 a[i] = an[i];
@@ -540,33 +543,24 @@ __device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t
             }
         }
     }
+    for (; s < n2; ++s) step2(lds4(ent + s * kES), lds4(ent + s * kES + 4));
     stamp(p, 8);
-    for (int s = 0; s < n3; s += 2) {
-        uint4 a[2], b[2], c[2];
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            a[i] = lds4(e3 + (s + i) * kE3);
-            b[i] = lds4(e3 + (s + i) * kE3 + 4);
-            c[i] = lds4(e3 + (s + i) * kE3 + 8);
-        }
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const uint32_t va = prmt(L.lo, a[i].x, L.hi), vb = prmt(L.lo, a[i].y, L.hi);
-            const uint32_t vc = prmt(L.lo, a[i].z, L.hi);
-            const uint32_t m1 = sgn(vb - va);
-            const uint32_t vab = pick(va, va ^ vb, m1);
-            const uint32_t ilo = pick(b[i].x, b[i].z, m1), ihi = pick(b[i].y, b[i].w, m1);
-            const uint32_t m2 = sgn(vc - vab);
-            L.lo += pick(ilo, ilo ^ c[i].x, m2);
-            L.hi += pick(ihi, ihi ^ c[i].y, m2);
-            const uint32_t gs = c[i].z, ga = gs & 0xffu, gb = (gs >> 8) & 0xffu, gc = (gs >> 16) & 0xffu;
-            const uint32_t gab = pick(ga, ga ^ gb, m1);
-            s_choice[c[i].w] = static_cast<int32_t>(pick(gab, gab ^ gc, m2));
-        }
+    for (; s < n2 + n3; ++s) {
+        const uint4 a = lds4(ent + s * kES), b = lds4(ent + s * kES + 4), c = lds4(ent + s * kES + 8);
+        const uint32_t va = prmt(L.lo, a.x, L.hi), vb = prmt(L.lo, a.y, L.hi), vc = prmt(L.lo, a.z, L.hi);
+        const uint32_t m1 = sgn(vb - va);
+        const uint32_t vab = pick(va, va ^ vb, m1);
+        const uint32_t ilo = pick(b.x, b.z, m1), ihi = pick(b.y, b.w, m1);
+        const uint32_t m2v = sgn(vc - vab);
+        L.lo += pick(ilo, ilo ^ c.x, m2v);
+        L.hi += pick(ihi, ihi ^ c.y, m2v);
+        const uint32_t gs = c.z, ga = gs & 0xffu, gb = (gs >> 8) & 0xffu, gc = (gs >> 16) & 0xffu;
+        const uint32_t gab = pick(ga, ga ^ gb, m1);
+        s_choice[c.w] = static_cast<int32_t>(pick(gab, gab ^ gc, m2v));
     }
     stamp(p, 9);
-    for (int s = 0; s < ng; ++s) {
-        const uint4 n0 = lds4(eg + s * kE3), n1 = lds4(eg + s * kE3 + 4), n2v = lds4(eg + s * kE3 + 8);
+    for (; s < m2; ++s) {
+        const uint4 n0 = lds4(ent + s * kES), n1 = lds4(ent + s * kES + 4), n2v = lds4(ent + s * kES + 8);
         const uint32_t nc[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
         Cand c[8];
 #pragma unroll
@@ -604,11 +598,10 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
     uint32_t *s_smask = reinterpret_cast<uint32_t *>(smem + L.smask);
     int32_t *s_sid = reinterpret_cast<int32_t *>(smem + L.sid);
     int32_t *s_L0 = reinterpret_cast<int32_t *>(smem + L.aux);
-    int32_t *s_hosted = s_L0 + kMaxG;  // active experts hosted per rank (bound on L[g])
     uint32_t *s_ent = reinterpret_cast<uint32_t *>(smem + L.ent);
+    const bool try_packed = (W == 1) && G <= 8;
 
-    int m2 = 0, n2 = 0, n3 = 0;
-    bool packed = false;
+    int m2 = 0;
     if (MODE != kFromOrder) {
         if (MODE == kFromIds) bad_min_warp0(L, smem, R, N);
         for (int base = 0; base < N; base += kThreads) {
@@ -616,17 +609,6 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
             const int e = base + tid;
             const bool valid = e < N;
             uint32_t t = 0;
-            if (valid) {
-                if (MODE == kFromIds) {
-#pragma unroll 4
-                    for (uint32_t r = 0; r < R; ++r) t += static_cast<uint32_t>(s_part[r * L.NP + e]);
-                } else {
-                    const int64_t tl = p.loads_in[e];
-                    if (tl < 0 || tl > 0xffffffffLL) misc[M_LOADERR] = 1;
-                    t = static_cast<uint32_t>(tl);
-                }
-                s_T[e] = t;
-            }
             uint32_t mw[W];
             int r = 0;
 #pragma unroll
@@ -634,52 +616,38 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
                 mw[j] = valid ? s_mask[e * W + j] : 0u;
                 r += __popc(mw[j]);
             }
-            if (base == 0) stamp(p, 14);
+            if (valid) {
+                if (MODE == kFromIds) {
+#pragma unroll 4
+                    for (uint32_t q = 0; q < R; ++q) t += static_cast<uint32_t>(s_part[q * L.NP + e]);
+                } else {
+                    const int64_t tl = p.loads_in[e];
+                    if (tl < 0 || tl > 0xffffffffLL) misc[M_LOADERR] = 1;
+                    t = static_cast<uint32_t>(tl);
+                }
+                s_T[e] = t;
+            }
             const bool active = t > 0;
+            const bool multi = active && r >= 2;
+            // compact replicated active experts first (any order: the sort ranks
+            // them); the segment atomic's latency overlaps the classification below
+            const unsigned bm = __ballot_sync(kFull, multi);
+            int seg = 0;
+            if (lane == 0 && bm) seg = atomicAdd(&misc[M_M2], __popc(bm));
+            if (base == 0) stamp(p, 14);
             if (active && r == 0) atomicMin(&misc[M_NOREP], e);
             const bool forced = active && r == 1;
-            const bool multi = active && r >= 2;
             int g1 = -1;
             if (forced) {
 #pragma unroll
                 for (int j = W - 1; j >= 0; --j)
                     if (mw[j]) g1 = 32 * j + __ffs(mw[j]) - 1;
-            }
-            if (valid) s_choice[e] = g1;
-            if (base == 0) stamp(p, 15);
-            // forced prefix: per-rank counts of single-replica active experts.  Their
-            // order is irrelevant: each lands on its only replica.
-            // Also count active experts hosted per rank: max <= 255 admits the packed greedy.
-            if (W == 1) {
-                int cnt = 0, host = 0;
-                for (int g = 0; g < G; ++g) {
-                    const unsigned b = __ballot_sync(kFull, g1 == g);
-                    const unsigned h = __ballot_sync(kFull, active && ((mw[0] >> g) & 1u));
-                    if (lane == g) {
-                        cnt = __popc(b);
-                        host = __popc(h);
-                    }
-                }
-                if (lane < G) {
-                    if (cnt) atomicAdd(&s_L0[lane], cnt);
-                    if (host) atomicAdd(&s_hosted[lane], host);
-                }
-            } else if (forced) {
+                // forced prefix: the single-replica experts' order is irrelevant
+                // (SURVEY.md App. A): each lands on its only replica
                 atomicAdd(&s_L0[g1], 1);
             }
-            // compact replicated active experts (any order: the sort ranks them)
-            if (base == 0) stamp(p, 16);
-            const unsigned bm = __ballot_sync(kFull, multi);
-            int seg = 0;
-            if (lane == 0 && bm) seg = atomicAdd(&misc[M_M2], __popc(bm));
-            const unsigned b2 = __ballot_sync(kFull, multi && r == 2);
-            const unsigned b3 = __ballot_sync(kFull, multi && r == 3);
-            if (lane == 0) {
-                if (b2) atomicAdd(&misc[M_N2], __popc(b2));
-                if (b3) atomicAdd(&misc[M_N3], __popc(b3));
-            }
+            if (valid) s_choice[e] = g1;
             seg = __shfl_sync(kFull, seg, 0);
-            if (base == 0) stamp(p, 17);
             if (multi) {
                 const int off = seg + __popc(bm & lanemask_lt());
                 // canonical key (routing.py:84-86): r asc, T desc, id asc
@@ -687,6 +655,7 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
                               static_cast<uint64_t>(e);
                 s_cand[off] = e;
             }
+            if (base == 0) stamp(p, 17);
         }
         stamp(p, 11);
         __syncthreads();
@@ -701,54 +670,39 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
             return false;
         }
         m2 = misc[M_M2];
-        n2 = misc[M_N2];
-        n3 = misc[M_N3];
-        if (W == 1 && G <= 8) {
-            int mx = 0;
-#pragma unroll
-            for (int g = 0; g < 8; ++g) mx = max(mx, g < G ? s_hosted[g] : 0);
-            packed = mx <= 126;
-        }
-        if (tid < 8) s_keys[m2 + tid] = ~0ull;  // pad for the pairwise scan
+        if (tid < 16) s_keys[m2 + tid] = ~0ull;  // pad for the paired scan
         __syncthreads();
         stamp(p, 4);
-        // ---- rank-by-count sort: one thread per replicated expert, broadcast key reads
-        uint32_t *e2 = s_ent;
-        uint32_t *e3 = e2 + (align_up(n2, 4) + 4) * kE2;
-        uint32_t *eg = e3 + align_up(n3, 2) * kE3;
-        // four threads per candidate: each scans every 4th key pair, quad shuffle-sum
+        // ---- rank-by-count sort: four threads per candidate scan every 4th key
+        // pair with broadcast loads, quad shuffle-sum; the candidate's entries are
+        // written at slot = rank (packed layout for G <= 8, SoA masks always)
         for (int c0 = 0; c0 < m2; c0 += kThreads / 4) {
             const int c = c0 + (tid >> 2), part = tid & 3;
             const uint64_t kc = (c < m2) ? s_keys[c] : 0ull;
-            int rk = 0;
-#pragma unroll 4
-            for (int c2 = 2 * part; c2 < m2; c2 += 8) {
-                const ulonglong2 kk = *reinterpret_cast<const ulonglong2 *>(s_keys + c2);
-                rk += (kk.x < kc) + (kk.y < kc);
+            // four independent counters: no compare -> add dependency chain
+            int r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+#pragma unroll 2
+            for (int c2 = 2 * part; c2 < m2; c2 += 16) {
+                const ulonglong2 k0 = *reinterpret_cast<const ulonglong2 *>(s_keys + c2);
+                const ulonglong2 k1 = *reinterpret_cast<const ulonglong2 *>(s_keys + c2 + 8);
+                r0 += k0.x < kc;
+                r1 += k0.y < kc;
+                r2 += k1.x < kc;
+                r3 += k1.y < kc;
             }
+            int rk = (r0 + r1) + (r2 + r3);
             rk += __shfl_xor_sync(kFull, rk, 1);
             rk += __shfl_xor_sync(kFull, rk, 2);
             if (c >= m2 || part != 0) continue;
             if (c == 0) stamp(p, 13);
             const int e = s_cand[c];
-            if (packed) {
-                const int r = static_cast<int>(kc >> 56);
-                if (rk < n2) packed_entry(e2 + rk * kE2, 2, s_mask[e], e);
-                else if (rk < n2 + n3) packed_entry(e3 + (rk - n2) * kE3, 3, s_mask[e], e);
-                else packed_entry(eg + (rk - n2 - n3) * kEG, r, s_mask[e], e);
-            } else {
+            const int r = static_cast<int>(kc >> 56);
 #pragma unroll
-                for (int j = 0; j < W; ++j) s_smask[j * N + rk] = s_mask[e * W + j];
-                s_sid[rk] = e;
-            }
-        }
-        if (packed && tid < 8) {  // no-op padding (zero increments, dummy choice slot N)
-            uint32_t *z2 = e2 + (n2 + tid) * kE2;
-            if (n2 + tid < align_up(n2, 4) + 4)
-                for (int w = 0; w < kE2; ++w) z2[w] = (w == 7) ? static_cast<uint32_t>(N) : 0u;
-            uint32_t *z3 = e3 + (n3 + tid) * kE3;
-            if (tid < 4 && n3 + tid < align_up(n3, 2))
-                for (int w = 0; w < kE3; ++w) z3[w] = (w == 11) ? static_cast<uint32_t>(N) : 0u;
+            for (int j = 0; j < W; ++j) s_smask[j * N + rk] = s_mask[e * W + j];
+            s_sid[rk] = e;
+            if (try_packed) packed_entry(s_ent + rk * kES, r, s_mask[e], e);
+            if (r == 2) atomicMax(&misc[M_N2], rk + 1);
+            if (r <= 3) atomicMax(&misc[M_N3], rk + 1);  // end of the r=3 segment
         }
     } else {
         // caller-supplied order (metro-parallel): single-replica experts included
@@ -777,89 +731,101 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
     __syncthreads();
     stamp(p, 5);
 
-    if (W == 1 && packed) {
+    bool done = false;
+    if (MODE != kFromOrder && try_packed) {
+        // Packed greedy (thread 0).  Valid iff every final counter is <= 126: the
+        // counters only grow, so no byte ever crossed into the sign bit.
         if (tid == 0) {
             PackedL Lp;
             Lp.lo = Lp.hi = 0;
+            int assigned = m2;
+            bool ok = true;
             for (int g = 0; g < G; ++g) {
-                const uint32_t v = static_cast<uint32_t>(s_L0[g]) << (8 * (g & 3));
+                const int c = s_L0[g];
+                ok = ok && c <= 126;
+                assigned += c;
+                const uint32_t v = static_cast<uint32_t>(c) << (8 * (g & 3));
                 if (g < 4) Lp.lo += v;
                 else Lp.hi += v;
             }
-            uint32_t *e2 = s_ent;
-            uint32_t *e3 = e2 + (align_up(n2, 4) + 4) * kE2;
-            uint32_t *eg = e3 + align_up(n3, 2) * kE3;
-            Lp = packed_greedy(p, e2, n2, e3, n3, eg, m2 - n2 - n3, s_choice, Lp);
-            s_L0[0] = static_cast<int32_t>(Lp.lo);
-            s_L0[1] = static_cast<int32_t>(Lp.hi);
+            const int n2 = misc[M_N2], n3 = misc[M_N3] - n2;
+            if (ok) Lp = packed_greedy(p, s_ent, n2, n3, m2, s_choice, Lp);
+            // every final counter <= 126 (no byte reached the sign bit; counters only
+            // grow) and the byte sum equals the assignments (no byte wrapped past 255)
+            ok = ok && ((Lp.lo | Lp.hi) & 0x80808080u) == 0 && ((Lp.lo + 0x01010101u) & 0x80808080u) == 0 &&
+                 ((Lp.hi + 0x01010101u) & 0x80808080u) == 0 &&
+                 __dp4a(Lp.lo, 0x01010101u, __dp4a(Lp.hi, 0x01010101u, 0u)) == static_cast<uint32_t>(assigned);
+            misc[M_PACKED_OK] = ok ? 1 : 0;
+            if (ok && writer) {
+                uint32_t mx = 0;
+                for (int g = 0; g < G; ++g) {
+                    const uint32_t c = ((g < 4 ? Lp.lo : Lp.hi) >> (8 * (g & 3))) & 0xffu;
+                    p.rank_counts[g] = static_cast<int32_t>(c);
+                    mx = max(mx, c);
+                }
+                *p.lam = static_cast<int32_t>(mx);
+            }
         }
         __syncthreads();
-        if (warp == 0) {
-            const uint32_t word = static_cast<uint32_t>(s_L0[lane >= 4 ? 1 : 0]);
-            const uint32_t c = lane < G ? ((word >> (8 * (lane & 3))) & 0xffu) : 0u;
-            if (writer && lane < G) p.rank_counts[lane] = static_cast<int32_t>(c);
-            const uint32_t mx = __reduce_max_sync(kFull, c);
-            if (writer && lane == 0) *p.lam = static_cast<int32_t>(mx);
-        }
-        stamp(p, 6);
-        return true;
+        done = misc[M_PACKED_OK] != 0;
     }
-
-    // ---- serial greedy (routing.py:94-101) in warp 0, any G <= 128.
-    // Lane owns ranks g = lane + 32 k as packed keys (L << 8 | g): the warp-wide
-    // min over candidate lanes is "smallest L, then smallest g" -- the
-    // reference's ascending scan with strict '<'.  Per chunk of 32 steps the
-    // candidacy bits are transposed with ballots (lane g gets bit s of step s),
-    // so the chain SEL -> redux.min -> ISETP -> IADD touches no memory.
-    if (warp == 0) {
-        uint32_t Lk[W];
-#pragma unroll
-        for (int k = 0; k < W; ++k) {
-            const int g = lane + 32 * k;
-            Lk[k] = (g < G) ? ((static_cast<uint32_t>(s_L0[g]) << 8) | static_cast<uint32_t>(g)) : 0xffffffffu;
-        }
-        for (int base = 0; base < m2; base += 32) {
-            const int j = base + lane;
-            const bool v = j < m2;
-            uint32_t cb[W];
+    if (!done) {
+        // ---- serial greedy (routing.py:94-101) in warp 0, any G <= 128.
+        // Lane owns ranks g = lane + 32 k as packed keys (L << 8 | g): the warp-wide
+        // min over candidate lanes is "smallest L, then smallest g" -- the
+        // reference's ascending scan with strict '<'.  Per chunk of 32 steps the
+        // candidacy bits are transposed with ballots (lane g gets bit s of step s),
+        // so the chain SEL -> redux.min -> ISETP -> IADD touches no memory.
+        if (warp == 0) {
+            uint32_t Lk[W];
 #pragma unroll
             for (int k = 0; k < W; ++k) {
-                const uint32_t m = v ? s_smask[k * N + j] : 0u;
-                cb[k] = 0;
-                const int gk = min(32, G - 32 * k);
-                for (int b = 0; b < gk; ++b) {
-                    const unsigned bb = __ballot_sync(kFull, (m >> b) & 1u);
-                    if (lane == b) cb[k] = bb;
+                const int g = lane + 32 * k;
+                Lk[k] = (g < G) ? ((static_cast<uint32_t>(s_L0[g]) << 8) | static_cast<uint32_t>(g)) : 0xffffffffu;
+            }
+            for (int base = 0; base < m2; base += 32) {
+                const int j = base + lane;
+                const bool v = j < m2;
+                uint32_t cb[W];
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    const uint32_t m = v ? s_smask[k * N + j] : 0u;
+                    cb[k] = 0;
+                    const int gk = min(32, G - 32 * k);
+                    for (int b = 0; b < gk; ++b) {
+                        const unsigned bb = __ballot_sync(kFull, (m >> b) & 1u);
+                        if (lane == b) cb[k] = bb;
+                    }
+                }
+                const int myid = v ? s_sid[j] : 0;
+                const int steps = min(32, m2 - base);
+                uint32_t wmine = 0;
+#pragma unroll
+                for (int s = 0; s < 32; ++s) {
+                    if (s >= steps) break;
+                    uint32_t val = 0xffffffffu;
+#pragma unroll
+                    for (int k = 0; k < W; ++k) val = ((cb[k] >> s) & 1u) ? min(val, Lk[k]) : val;
+                    const uint32_t win = __reduce_min_sync(kFull, val);
+#pragma unroll
+                    for (int k = 0; k < W; ++k) Lk[k] += (Lk[k] == win) ? 256u : 0u;
+                    wmine = (lane == s) ? win : wmine;
+                }
+                if (v) s_choice[myid] = static_cast<int32_t>(wmine & 0xffu);
+            }
+            uint32_t mx = 0;
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                const int g = lane + 32 * k;
+                if (g < G) {
+                    const uint32_t c = Lk[k] >> 8;
+                    if (writer) p.rank_counts[g] = static_cast<int32_t>(c);
+                    mx = max(mx, c);
                 }
             }
-            const int myid = v ? s_sid[j] : 0;
-            const int steps = min(32, m2 - base);
-            uint32_t wmine = 0;
-#pragma unroll
-            for (int s = 0; s < 32; ++s) {
-                if (s >= steps) break;
-                uint32_t val = 0xffffffffu;
-#pragma unroll
-                for (int k = 0; k < W; ++k) val = ((cb[k] >> s) & 1u) ? min(val, Lk[k]) : val;
-                const uint32_t win = __reduce_min_sync(kFull, val);
-#pragma unroll
-                for (int k = 0; k < W; ++k) Lk[k] += (Lk[k] == win) ? 256u : 0u;
-                wmine = (lane == s) ? win : wmine;
-            }
-            if (v) s_choice[myid] = static_cast<int32_t>(wmine & 0xffu);
+            mx = __reduce_max_sync(kFull, mx);
+            if (writer && lane == 0) *p.lam = static_cast<int32_t>(mx);
         }
-        uint32_t mx = 0;
-#pragma unroll
-        for (int k = 0; k < W; ++k) {
-            const int g = lane + 32 * k;
-            if (g < G) {
-                const uint32_t c = Lk[k] >> 8;
-                if (writer) p.rank_counts[g] = static_cast<int32_t>(c);
-                mx = max(mx, c);
-            }
-        }
-        mx = __reduce_max_sync(kFull, mx);
-        if (writer && lane == 0) *p.lam = static_cast<int32_t>(mx);
     }
     __syncthreads();
     stamp(p, 6);
@@ -1448,29 +1414,50 @@ size_t metro_host_workspace_bytes(int64_t num_pairs, int32_t N, int32_t G) {
            (size_t)num_pairs * 4 + 256;
 }
 
-int metro_route_host_v1(const int32_t *ids_host, int64_t num_pairs, const uint32_t *mask_dev,
-                        int32_t N, int32_t G, void *ws, int32_t *host_out, int32_t *pair_rank_host,
-                        int32_t cluster_ctas, void *stream) {
-    if (!ws || !host_out || !mask_dev || (num_pairs > 0 && !ids_host) || num_pairs < 0) return METRO_EARG;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    unsigned char *base = static_cast<unsigned char *>(ws);
-    int32_t *d_ids = reinterpret_cast<int32_t *>(base);
-    int32_t *d_out = reinterpret_cast<int32_t *>(base + ws_ids_bytes(num_pairs));
-    int32_t *d_pr = reinterpret_cast<int32_t *>(reinterpret_cast<unsigned char *>(d_out) +
-                                                ((ws_out_words(N, G) * 4 + 255) & ~(size_t)255));
-    cudaError_t e;
-    if (num_pairs > 0) {
-        e = cudaMemcpyAsync(d_ids, ids_host, (size_t)num_pairs * 4, cudaMemcpyHostToDevice, s);
-        if (e != cudaSuccess) return cuda_fail(e);
+static bool device_accessible(const void *p) {
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
     }
-    int rc = metro_route_v1(d_ids, num_pairs, mask_dev, N, G, nullptr, d_out + 8 + G, d_out + 8,
-                            d_out + 4, pair_rank_host ? d_pr : nullptr, d_out, cluster_ctas, stream);
-    if (rc) return rc;
-    e = cudaMemcpyAsync(host_out, d_out, ws_out_words(N, G) * 4, cudaMemcpyDeviceToHost, s);
-    if (e != cudaSuccess) return cuda_fail(e);
-    if (pair_rank_host && num_pairs > 0) {
-        e = cudaMemcpyAsync(pair_rank_host, d_pr, (size_t)num_pairs * 4, cudaMemcpyDeviceToHost, s);
+    return (attr.type == cudaMemoryTypeHost || attr.type == cudaMemoryTypeManaged) && attr.devicePointer == p;
+}
+
+int metro_route_host_v1(const int32_t *ids_host, int64_t num_pairs, const uint32_t *mask_dev, int32_t N,
+                        int32_t G, void *ws, int32_t *host_out, int32_t *pair_rank_host, int32_t cluster_ctas,
+                        int32_t flags, void *stream) {
+    if (!host_out || !mask_dev || (num_pairs > 0 && !ids_host) || num_pairs < 0) return METRO_EARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if (flags & METRO_HOST_ZEROCOPY) {
+        // the kernel reads the ids from and writes the results to pinned host memory
+        // directly (PCIe reads/posted writes inside the launch): no copy engines
+        if ((num_pairs > 0 && !device_accessible(ids_host)) || !device_accessible(host_out) ||
+            (pair_rank_host && !device_accessible(pair_rank_host)))
+            return METRO_EARG;
+        int rc = metro_route_v1(ids_host, num_pairs, mask_dev, N, G, nullptr, host_out + 8 + G, host_out + 8,
+                                host_out + 4, pair_rank_host, host_out, cluster_ctas, stream);
+        if (rc) return rc;
+    } else {
+        if (!ws) return METRO_EARG;
+        unsigned char *base = static_cast<unsigned char *>(ws);
+        int32_t *d_ids = reinterpret_cast<int32_t *>(base);
+        int32_t *d_out = reinterpret_cast<int32_t *>(base + ws_ids_bytes(num_pairs));
+        int32_t *d_pr = reinterpret_cast<int32_t *>(reinterpret_cast<unsigned char *>(d_out) +
+                                                    ((ws_out_words(N, G) * 4 + 255) & ~(size_t)255));
+        if (num_pairs > 0) {
+            e = cudaMemcpyAsync(d_ids, ids_host, (size_t)num_pairs * 4, cudaMemcpyHostToDevice, s);
+            if (e != cudaSuccess) return cuda_fail(e);
+        }
+        int rc = metro_route_v1(d_ids, num_pairs, mask_dev, N, G, nullptr, d_out + 8 + G, d_out + 8, d_out + 4,
+                                pair_rank_host ? d_pr : nullptr, d_out, cluster_ctas, stream);
+        if (rc) return rc;
+        e = cudaMemcpyAsync(host_out, d_out, ws_out_words(N, G) * 4, cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) return cuda_fail(e);
+        if (pair_rank_host && num_pairs > 0) {
+            e = cudaMemcpyAsync(pair_rank_host, d_pr, (size_t)num_pairs * 4, cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) return cuda_fail(e);
+        }
     }
     e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(e);

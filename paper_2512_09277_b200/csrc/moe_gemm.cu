@@ -1,0 +1,368 @@
+// moe_gemm.cu -- K3: grouped expert GEMM for the memory-bound MoE decode FFN
+// on 5th-generation tensor cores (tcgen05 + TMEM + TMA), sm_100a.
+//
+// Purpose on this path (BASELINE.json north_star (4)):
+// show that fewer activated replicas means fewer weight bytes pulled from HBM.
+// The reference only models it: memory_time = (lambda * expert_bytes + ...) / HBM
+// (/root/reference/pkg/src/eproute/costmodel.py:83-94).
+//
+// Swap-AB: in decode the token count per expert is small, so the weight matrix
+// is the MMA "A" operand on M (128 rows per tile) and the tokens are "B" on N:
+//     Y[t, m] = sum_k W[e][m, k] * X[t, k]      (D[m, n] = A[m, k] * B[n, k], both K-major)
+// One work item = (expert slot e, 128-row block of W, up to 256 tokens of e).
+// Persistent CTAs (one per SM), warp-specialised:
+//   warp 4: TMA producer (W tile 128x64, X tile nb x 64, 128B swizzle, mbarrier ring)
+//   warp 5: MMA issuer (one thread; tcgen05.mma kind::f16, fp32 accumulators in TMEM,
+//           double-buffered so the epilogue of item i overlaps the MMAs of item i+1)
+//   warps 0-3: epilogue (tcgen05.ld 32x32b -> bf16 -> coalesced stores)
+// Weights are streamed exactly once per item; the kernel is HBM-bound.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "../../include/moe_gemm.h"
+
+namespace moe {
+
+constexpr int BM = 128;        // weight rows per tile (UMMA M)
+constexpr int BK = 64;         // bf16 elements per 128-byte swizzled row
+constexpr int MAXN = 256;      // tokens per item (UMMA N <= 256)
+constexpr int STAGES = 4;
+constexpr int kThreads = 192;  // 4 epilogue warps + TMA warp + MMA warp
+constexpr int A_BYTES = BM * BK * 2;    // 16 KB
+constexpr int B_BYTES = MAXN * BK * 2;  // 32 KB
+constexpr int NMAPS = 5;                // X maps with box heights 16, 32, 64, 128, 256
+constexpr int kSmem = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+constexpr int TMEM_COLS = 512;          // 2 accumulators x 256 fp32 columns
+
+struct Item {
+    int e, m_blk, t0, n;
+};
+
+struct Params {
+    const Item *items;
+    int n_items;
+    int K;
+    __nv_bfloat16 *Y;
+    int ldy;
+};
+
+struct Maps {
+    CUtensorMap w;          // [E][M][K]
+    CUtensorMap x[NMAPS];   // [T][K], box heights 16 << i
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, uint64_t *b) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(b))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *b) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(b))
+        : "memory");
+}
+// UMMA shared-memory descriptor, K-major, 128-byte swizzle: rows of 128 B, 8-row
+// atoms of 1024 B (SBO), LBO unused (1), version 1 (sm100), layout type 2.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (64ull << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+// instruction descriptor: D f32, A/B bf16, both K-major, M = 128, N = n
+__device__ __forceinline__ uint32_t idesc_bf16(int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+           (static_cast<uint32_t>(BM >> 4) << 24);
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t *b) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+#define TMEM_LD_X32(taddr, v)                                                                                    \
+    asm volatile(                                                                                                \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "   \
+        "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"       \
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),        \
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),   \
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),              \
+          "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),              \
+          "=r"(v[30]), "=r"(v[31])                                                                                \
+        : "r"(taddr))
+
+__device__ __forceinline__ int map_index(int n) {  // smallest box height >= n
+    int i = 0;
+    while (i < NMAPS - 1 && (16 << i) < n) ++i;
+    return i;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_constant__ Maps maps, const Params p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char *sA = smem;
+    unsigned char *sB = smem + STAGES * A_BYTES;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sB + STAGES * B_BYTES);
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;   // [2]
+    uint64_t *tempty = tfull + 2;       // [2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kblocks = p.K / BK;
+
+    if (warp == 4 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.w)) : "memory");
+    }
+    if (warp == 5) {  // TMEM allocation by one full warp
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 4) {
+        // ---------------- TMA producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+                const Item item = p.items[it];
+                const int mi = map_index(item.n);
+                const uint32_t bbytes = static_cast<uint32_t>((16 << mi) * BK * 2);
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], A_BYTES + bbytes);
+                    tma_load_3d(sA + stage * A_BYTES, &maps.w, kb * BK, item.m_blk * BM, item.e, &full[stage]);
+                    tma_load_2d(sB + stage * B_BYTES, &maps.x[mi], kb * BK, item.t0, &full[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer (one thread)
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int local = 0;
+            for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++local) {
+                const Item item = p.items[it];
+                const int acc = local & 1;
+                const uint32_t aphase = (local >> 1) & 1;
+                mbar_wait(&tempty[acc], aphase ^ 1);
+                tc_fence_after();
+                const int nmma = (item.n + 15) & ~15;
+                const uint32_t idesc = idesc_bf16(nmma);
+                const uint32_t dcol = tmem_base + static_cast<uint32_t>(acc * MAXN);
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        umma_bf16(dcol, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc,
+                                  (kb | k) != 0 ? 1u : 0u);
+                    umma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+            }
+        }
+    } else {
+        // ---------------- epilogue: warps 0-3 own TMEM lanes 32w .. 32w+31 (= W rows)
+        int local = 0;
+        for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++local) {
+            const Item item = p.items[it];
+            const int acc = local & 1;
+            const uint32_t aphase = (local >> 1) & 1;
+            mbar_wait(&tfull[acc], aphase);
+            tc_fence_after();
+            const int row = item.m_blk * BM + warp * 32 + lane;
+            const uint32_t tbase = tmem_base + static_cast<uint32_t>(acc * MAXN) + (static_cast<uint32_t>(warp * 32) << 16);
+            for (int c = 0; c < item.n; c += 32) {
+                uint32_t v[32];
+                TMEM_LD_X32(tbase + static_cast<uint32_t>(c), v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const int lim = min(32, item.n - c);
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (j < lim)
+                        p.Y[static_cast<int64_t>(item.t0 + c + j) * p.ldy + row] =
+                            __float2bfloat16_rn(__uint_as_float(v[j]));
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 5)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                     : "memory");
+}
+
+// H[t, i] = silu(GU[t, i]) * GU[t, I + i]   (gate | up halves of the first projection)
+__global__ void silu_mul_kernel(const __nv_bfloat16 *__restrict__ gu, int T, int I, __nv_bfloat16 *__restrict__ h) {
+    const int64_t total = static_cast<int64_t>(T) * I;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t t = idx / I, i = idx - t * I;
+        const float g = __bfloat162float(gu[t * 2 * I + i]);
+        const float u = __bfloat162float(gu[t * 2 * I + I + i]);
+        h[idx] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u);
+    }
+}
+
+// ---------------------------------------------------------------- host
+static thread_local int g_err = 0;
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    });
+    return fn;
+}
+
+static bool encode(CUtensorMap *m, void *base, int rank, const cuuint64_t *dims, const cuuint64_t *strides,
+                   const cuuint32_t *box) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint32_t es[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, base, dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace moe
+
+using namespace moe;
+
+extern "C" {
+
+METRO_API int moe_grouped_gemm_v1(const void *W, int32_t E, int32_t M, int32_t K, const void *X, int32_t T,
+                        const int32_t *items, int32_t n_items, void *Y, int32_t num_ctas, void *stream) {
+    if (!W || !X || !Y || (!items && n_items > 0) || E < 1 || M < BM || K < BK || T < 1 || n_items < 0)
+        return METRO_EARG;
+    if (M % BM || K % BK) return METRO_EDIMS;
+    if (n_items == 0) return METRO_OK;
+    Maps maps;
+    const cuuint64_t wdims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(E)};
+    const cuuint64_t wstr[2] = {static_cast<cuuint64_t>(K) * 2, static_cast<cuuint64_t>(M) * K * 2};
+    const cuuint32_t wbox[3] = {BK, BM, 1};
+    if (!encode(&maps.w, const_cast<void *>(W), 3, wdims, wstr, wbox)) return METRO_ECUDA;
+    const cuuint64_t xdims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(T)};
+    const cuuint64_t xstr[1] = {static_cast<cuuint64_t>(K) * 2};
+    for (int i = 0; i < NMAPS; ++i) {
+        const cuuint32_t xbox[2] = {BK, static_cast<cuuint32_t>(16 << i)};
+        if (!encode(&maps.x[i], const_cast<void *>(X), 2, xdims, xstr, xbox)) return METRO_ECUDA;
+    }
+    static std::once_flag attr;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr, [] {
+        attr_err = cudaFuncSetAttribute(moe_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    });
+    if (attr_err != cudaSuccess) {
+        g_err = attr_err;
+        return METRO_ECUDA;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = num_ctas > 0 ? num_ctas : (n_items < sms ? n_items : sms);
+    Params prm;
+    prm.items = reinterpret_cast<const Item *>(items);
+    prm.n_items = n_items;
+    prm.K = K;
+    prm.Y = static_cast<__nv_bfloat16 *>(Y);
+    prm.ldy = M;
+    moe_gemm_kernel<<<grid, kThreads, kSmem, static_cast<cudaStream_t>(stream)>>>(maps, prm);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        g_err = e;
+        return METRO_ECUDA;
+    }
+    return METRO_OK;
+}
+
+METRO_API int moe_silu_mul_v1(const void *GU, int32_t T, int32_t I, void *H, void *stream) {
+    if (!GU || !H || T < 0 || I < 1) return METRO_EARG;
+    if (T == 0) return METRO_OK;
+    const int64_t total = static_cast<int64_t>(T) * I;
+    const int grid = static_cast<int>(total / 256 + 1 < 148 * 8 ? total / 256 + 1 : 148 * 8);
+    silu_mul_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const __nv_bfloat16 *>(GU), T, I, static_cast<__nv_bfloat16 *>(H));
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        g_err = e;
+        return METRO_ECUDA;
+    }
+    return METRO_OK;
+}
+
+METRO_API int moe_last_cuda_error(void) { return g_err; }
+
+}  // extern "C"

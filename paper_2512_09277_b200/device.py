@@ -196,14 +196,18 @@ def aggregate_loads_device(topk_ids: torch.Tensor, num_experts: int, cluster_cta
 class HostRouter:
     """End-to-end METRO from host (pinned) buffers through metro_route_host_v1.
 
-    Each call: H2D of the ids, the routing kernel, D2H of choice / rank_counts /
-    lam / status (+ pair_rank), stream synchronise -- the reference-facing call a
-    CPU-resident caller makes.
+    Each call moves the ids host -> device, routes, moves choice / rank_counts /
+    lam / status (+ pair_rank) device -> host and synchronises -- the
+    reference-facing call a CPU-resident caller makes.  ``zero_copy=True`` lets
+    the kernel read/write the pinned host buffers directly over PCIe (no copy
+    engine round trips); ``False`` uses explicit cudaMemcpyAsync H2D / D2H.
     """
 
-    def __init__(self, placement: DevicePlacement, max_pairs: int, cluster_ctas: int = 0):
+    def __init__(self, placement: DevicePlacement, max_pairs: int, cluster_ctas: int = 0,
+                 zero_copy: bool = True):
         self.placement = placement
         self.cluster_ctas = int(cluster_ctas)
+        self.flags = _native.HOST_ZEROCOPY if zero_copy else 0
         L = _native.lib()
         n, g = placement.num_experts, placement.num_ranks
         nbytes = L.metro_host_workspace_bytes(max_pairs, n, g)
@@ -222,7 +226,7 @@ class HostRouter:
             ids_host.data_ptr(), ids_host.numel(), p.mask.data_ptr(), p.num_experts, p.num_ranks,
             self.ws.data_ptr(), self.host_out.data_ptr(),
             None if pair_rank_host is None else pair_rank_host.data_ptr(), self.cluster_ctas,
-            self.stream.cuda_stream,
+            self.flags, self.stream.cuda_stream,
         )
         _native.check_rc(rc, "metro_route_host_v1")
         return self.host_out.numpy()

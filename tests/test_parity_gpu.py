@@ -185,6 +185,23 @@ def test_max_sizes():
     check_metro(ids, make_placement(256, 8, 1.5, 7).matrix, 16)
 
 
+def test_packed_greedy_fallback():
+    """Ranks hosting > 126 active experts leave the byte-packed greedy's range; the
+    kernel must detect it and fall back to the warp greedy (still bit-exact)."""
+    rng = np.random.default_rng(31)
+    for n, g in [(300, 2), (256, 2), (400, 4), (256, 8)]:
+        A = np.ones((n, g), dtype=np.int8)
+        ids = rng.integers(0, n, size=(2048, 8)).astype(np.int32)
+        for cl in (0, 1, 4):
+            check_metro(ids, A, cl)
+    # one rank hosting every expert (a counter could pass 255 without the guard)
+    A = np.zeros((256, 4), dtype=np.int8)
+    A[:, 0] = 1
+    A[::3, 1] = 1
+    ids = np.arange(256 * 8, dtype=np.int32).reshape(-1, 8) % 256
+    check_metro(ids, A, 0)
+
+
 def test_id_out_of_range_error():
     A = make_placement(128, 8, 1.5, 7).matrix
     ids = gen_zipf_topk(128, 8, 256, 1.2, 1)

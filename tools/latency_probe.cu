@@ -145,6 +145,61 @@ __global__ void probe(int64_t *out, uint32_t seed) {
     }
     // 18: sub -> prmt sign chain
     RUN("sub_sgn", { asm volatile("sub.u32 %0, %0, %1;" : "+r"(x) : "r"(y)); asm volatile("prmt.b32 %0, %0, 0, 0xBBBB;" : "+r"(x)); });
+    // 19: prmt -> add.cc (carry form, hoping for IADD3 on the ALU pipe)
+    {
+        uint32_t lo = x, hi = y;
+        t0 = clock64();
+        for (int i = 0; i < ITERS; ++i) {
+            uint32_t va;
+            asm volatile("prmt.b32 %0, %1, %2, 0x8881;" : "=r"(va) : "r"(lo), "r"(hi));
+            asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(lo) : "r"(va));
+        }
+        t1 = clock64();
+        if (threadIdx.x == 0) out[k] = t1 - t0;
+        k++;
+        x ^= lo;
+    }
+    // 20: r2 step with add.cc / sub.cc on the chain
+    {
+        uint32_t lo = x & 0x3f3f3f3f, hi = y & 0x3f3f3f3f, ia = 1, xa = 0x101;
+        t0 = clock64();
+        for (int i = 0; i < ITERS; ++i) {
+            uint32_t va, vb, m, pl, ph;
+            asm volatile("prmt.b32 %0, %1, %2, 0x8881;" : "=r"(va) : "r"(lo), "r"(hi));
+            asm volatile("prmt.b32 %0, %1, %2, 0xDDD5;" : "=r"(vb) : "r"(lo), "r"(hi));
+            asm volatile("sub.cc.u32 %0, %1, %2;" : "=r"(m) : "r"(vb), "r"(va));
+            asm volatile("prmt.b32 %0, %0, 0, 0xBBBB;" : "+r"(m));
+            asm volatile("lop3.b32 %0, %1, %2, %3, 0x78;" : "=r"(pl) : "r"(ia), "r"(xa), "r"(m));
+            asm volatile("lop3.b32 %0, %1, %2, %3, 0x78;" : "=r"(ph) : "r"(ia), "r"(xa), "r"(m));
+            asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(lo) : "r"(pl));
+            asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(hi) : "r"(ph));
+        }
+        t1 = clock64();
+        if (threadIdx.x == 0) out[k] = t1 - t0;
+        k++;
+        x ^= lo ^ hi;
+    }
+    // 21: same step, plain add/sub (for comparison without the mask lop3)
+    {
+        uint32_t lo = x & 0x3f3f3f3f, hi = y & 0x3f3f3f3f, ia = 1, xa = 0x101;
+        t0 = clock64();
+        for (int i = 0; i < ITERS; ++i) {
+            uint32_t va, vb, m, pl, ph;
+            asm volatile("prmt.b32 %0, %1, %2, 0x8881;" : "=r"(va) : "r"(lo), "r"(hi));
+            asm volatile("prmt.b32 %0, %1, %2, 0xDDD5;" : "=r"(vb) : "r"(lo), "r"(hi));
+            asm volatile("sub.u32 %0, %1, %2;" : "=r"(m) : "r"(vb), "r"(va));
+            asm volatile("prmt.b32 %0, %0, 0, 0xBBBB;" : "+r"(m));
+            asm volatile("lop3.b32 %0, %1, %2, %3, 0x78;" : "=r"(pl) : "r"(ia), "r"(xa), "r"(m));
+            asm volatile("lop3.b32 %0, %1, %2, %3, 0x78;" : "=r"(ph) : "r"(ia), "r"(xa), "r"(m));
+            asm volatile("add.u32 %0, %0, %1;" : "+r"(lo) : "r"(pl));
+            asm volatile("add.u32 %0, %0, %1;" : "+r"(hi) : "r"(ph));
+        }
+        t1 = clock64();
+        if (threadIdx.x == 0) out[k] = t1 - t0;
+        k++;
+        x ^= lo ^ hi;
+    }
+    // 22: r2 step using vadd-free 3-input iadd: lo = lo + pl + 0 via add.cc/addc
     if (threadIdx.x == 0) out[63] = x;
 }
 
@@ -158,7 +213,7 @@ int main() {
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
     const char *names[] = {"prmt", "iadd", "setp+pred_add", "setp+selp", "min.u32", "lop3", "shf", "redux.min",
                            "shfl.xor", "lds chase", "r2 step (pred add)", "r2 step (selp+add)", "min.u16x2",
-                           "add.u64", "imad", "r2 new (lop3 pick)", "r2 imad pick", "prmt->add", "sub->prmt sign"};
-    for (int i = 0; i < 19; ++i) printf("%-22s %6.2f cycles/iter\n", names[i], (double)h[i] / ITERS);
+                           "add.u64", "imad", "r2 new (lop3 pick)", "r2 imad pick", "prmt->add", "sub->prmt sign", "prmt->add.cc", "r2 step add.cc", "r2 step plain"};
+    for (int i = 0; i < 22; ++i) printf("%-22s %6.2f cycles/iter\n", names[i], (double)h[i] / ITERS);
     return 0;
 }

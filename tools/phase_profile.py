@@ -59,9 +59,8 @@ def main():
                           "to_sort": int(s[4] - s[12]), "rank_loop_t0": int(s[13] - s[4]),
                           "r2": int(s[8] - s[5]), "r3": int(s[9] - s[8]), "rgen": int(s[10] - s[9]),
                           "greedy_tail": int(s[6] - s[10]),
-                          "c_tsum": int(s[14] - s[3]), "c_classify": int(s[15] - s[14]),
-                          "c_ballots": int(s[16] - s[15]), "c_compact": int(s[17] - s[16]),
-                          "c_rest": int(s[11] - s[17])}
+                          "c_head": int(s[14] - s[3]), "c_body": int(s[17] - s[14]),
+                          "c_tail": int(s[11] - s[17])}
             # back-to-back graph replay over a pool of distinct batches > L2
             per = ids.numel() * 4
             P = max(64, (256 << 20) // per)
