@@ -66,6 +66,7 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU-baseline sample length")
     ap.add_argument("--e2e-steps", type=int, default=1000)
     ap.add_argument("--detail", default=None, help="write extra per-run detail JSON here")
+    ap.add_argument("--no-moe", action="store_true", help="skip the K3 expert-FFN measurement")
     return ap.parse_args()
 
 
@@ -462,6 +463,22 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
                          "achieved_gbs": recv / (ag_ms * 1e-3) / 1e9, "peak_gbs": 770.0,
                          "frac": recv / (ag_ms * 1e-3) / 1e9 / 770.0,
                          "peak_source": "measured peer copy, B200_PROFILING.md"}
+    if world == 1 and not args.no_moe and cfg["N"] == 256 and cfg["G"] == 8:
+        # BASELINE configs[4]: the bottleneck rank's expert FFN (K3, tcgen05) under the
+        # METRO vs EPLB routing of the same batches -> weight bytes vs activated replicas
+        sys.path.insert(0, os.path.join(REPO, "tools"))
+        import moe_layer_bench
+
+        m = moe_layer_bench.run(batches=2, reps=3, B=cfg["B"], ratio=cfg["ratio"])
+        res["moe_layer_k3"] = {
+            "what": "expert FFN (gate_up + silu*mul + down, bf16, D=7168 I=2048) on the rank with the most "
+                    "activated replicas; tcgen05 grouped GEMM streaming the activated experts' weights",
+            "metro": m["metro"], "eplb": m["eplb"],
+            "ffn_speedup_metro_vs_eplb": m["ffn_speedup_metro_vs_eplb"],
+            "weight_byte_ratio_eplb_over_metro": m["weight_byte_ratio_eplb_over_metro"],
+            "roofline": {"bound": "hbm", "achieved": m["metro"]["achieved_gbs"], "peak": m["peak_gbs"],
+                         "unit": "GB/s", "frac": m["metro"]["frac"], "kernel": "moe_gemm_kernel"},
+        }
     if world == 1:
         us, layers, outs = cpu_route_layers(A, batches, args.cpu_seconds)
         parity = all(int(o[3][0]) == lm for o, lm in zip(outs, lam_m))

@@ -78,7 +78,7 @@ struct Params {
 // The METRO sort/greedy scratch (keys, cand, smask, sid) aliases hist + part:
 // both are dead once the partial histograms have been reduced into T.
 struct Layout {
-    int mbar, misc, mask, ids, T, choice, aux, hist, part, keys, cand, smask, sid, ent, total;
+    int mbar, misc, mask, ids, T, choice, aux, hist, part, keys, cand, smask, sid, ent, rpart, total;
     int NP;  // partial-row stride (words): N + 2 (bad pair lo/hi) rounded to 4
 };
 
@@ -110,11 +110,12 @@ __host__ __device__ inline Layout make_layout(int kind, int N, int W, int R, int
     const int end1 = ids_mode ? align_up(L.part + R * L.NP * 4, 16) : L.part;
     L.keys = o;
     L.cand = align_up(L.keys + (N + 16) * 8, 16);
-    L.smask = align_up(L.cand + N * 4, 16);
-    L.sid = align_up(L.smask + N * W * 4, 16);
+    L.smask = L.cand;  // (unused: the warp greedy reads masks through sid)
+    L.sid = align_up(L.cand + N * 4, 16);
     L.ent = align_up(L.sid + N * 4, 16);
     // packed-greedy entries (W == 1 only), one slot per rank + readable padding
-    const int end2 = metro ? align_up(L.ent + (W == 1 ? (N + 16) * kES * 4 : 0), 16) : o;
+    L.rpart = align_up(L.ent + (W == 1 ? (N + 16) * kES * 4 : 0), 16);  // [4][N] partial ranks
+    const int end2 = metro ? align_up(L.rpart + 4 * N * 4, 16) : o;
     L.total = end1 > end2 ? end1 : end2;
     return L;
 }
@@ -184,6 +185,17 @@ __device__ __forceinline__ void dsmem_st(const void *local, uint32_t cta, uint32
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(local)), "r"(cta));
     asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(raddr), "r"(v) : "memory");
 }
+// Asynchronous 4-byte store into CTA `cta`'s shared memory (same offset as `local`
+// in ours) that completes `bytes` on that CTA's mbarrier at `local_bar`'s offset.
+__device__ __forceinline__ void st_async_b32(const void *local, uint32_t cta, uint32_t v, const void *local_bar) {
+    uint32_t raddr, rbar;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(local)), "r"(cta));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(local_bar)), "r"(cta));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(raddr), "r"(v),
+                 "r"(rbar)
+                 : "memory");
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -234,7 +246,8 @@ __device__ __forceinline__ StagePlan stage_plan(const Params &p, int64_t beg, in
 __device__ __forceinline__ void stage_issue(const Params &p, const Layout &L, unsigned char *smem, int64_t beg,
                                             const StagePlan &s) {
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + L.mbar);
-    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);  // partial-histogram exchange (st.async from the peer CTAs)
+    mbar_init(bar, 1);      // TMA staging (its init fence covers both)
     const uint32_t bytes = (s.mask_bulk ? s.mask_words * 4u : 0u) + (s.ids_bulk ? s.body * 4u : 0u);
     mbar_arrive_expect_tx(bar, bytes);
     if (s.mask_bulk) bulk_g2s(smem + L.mask, p.mask, s.mask_words * 4u, bar);
@@ -333,9 +346,17 @@ __device__ void histogram_push(const Params &p, const Layout &L, unsigned char *
     __syncthreads();
     stamp(p, 2);
 
-    // all CTAs of the cluster have started (they arrived at kernel entry) before
-    // anyone writes into a peer's shared memory
-    if (R > 1) cluster_wait();
+    // The peers' exchange mbarriers are initialised (every CTA arrived, with release
+    // semantics, after its thread 0 initialised them) before anyone stores into a
+    // peer.  Each partial goes out as st.async completing bytes on the receiver's
+    // mbarrier: no release fence round trip and no cluster barrier; a CTA only
+    // waits for the bytes it receives.
+    uint64_t *xbar = reinterpret_cast<uint64_t *>(smem + L.mbar) + 1;
+    if (R > 1) {
+        cluster_wait();
+        if (tid == 0) mbar_arrive_expect_tx(xbar, (R - 1) * static_cast<uint32_t>(N + 2) * 4u);
+    }
+    stamp(p, 20);
     int32_t *row = s_part + rank * L.NP;
     for (int e = tid; e < N; e += kThreads) {
         int s = 0;
@@ -357,20 +378,15 @@ __device__ void histogram_push(const Params &p, const Layout &L, unsigned char *
 #pragma unroll 4
             for (int w = 0; w < kWarps; ++w) s += s_hist[w * N + e];
         }
-        row[e] = s;
-        for (uint32_t d = 1; d < R; ++d) dsmem_st(row + e, (rank + d) % R, static_cast<uint32_t>(s));
+        row[e] = s;  // read back only by this thread (same e mapping downstream)
+        for (uint32_t d = 1; d < R; ++d) st_async_b32(row + e, (rank + d) % R, static_cast<uint32_t>(s), xbar);
     }
-    if (tid < 2) {
+    if (tid < 2 && R > 1) {
         const int32_t v = misc[M_BAD_LO + tid];
-        row[N + tid] = v;
-        for (uint32_t d = 1; d < R; ++d) dsmem_st(row + N + tid, (rank + d) % R, static_cast<uint32_t>(v));
+        for (uint32_t d = 1; d < R; ++d) st_async_b32(row + N + tid, (rank + d) % R, static_cast<uint32_t>(v), xbar);
     }
-    if (R > 1) {
-        cluster_arrive_release();
-        cluster_wait();
-    } else {
-        __syncthreads();
-    }
+    stamp(p, 18);
+    if (R > 1) mbar_wait(xbar, 0);
     stamp(p, 3);
 }
 
@@ -380,8 +396,12 @@ __device__ __forceinline__ void bad_min_warp0(const Layout &L, unsigned char *sm
     int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
     const int32_t *s_part = reinterpret_cast<const int32_t *>(smem + L.part);
     const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
     uint32_t lo = kBadLo, hi = kBadHi;
-    if (static_cast<uint32_t>(lane) < R) {
+    if (static_cast<uint32_t>(lane) == rank) {  // own partial: never written to the row
+        lo = static_cast<uint32_t>(misc[M_BAD_LO]);
+        hi = static_cast<uint32_t>(misc[M_BAD_HI]);
+    } else if (static_cast<uint32_t>(lane) < R) {
         lo = static_cast<uint32_t>(s_part[lane * L.NP + N]);
         hi = static_cast<uint32_t>(s_part[lane * L.NP + N + 1]);
     }
@@ -518,29 +538,52 @@ __device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t
         const uint32_t gs = b.z;
         s_choice[b.w] = static_cast<int32_t>(pick(gs & 0xffu, (gs ^ (gs >> 8)) & 0xffu, m));
     };
+    // Two consecutive r=2 steps (a, b) then (c, d) in one dependency chain: all four
+    // loads are extracted from the same L, and step 2 corrects its difference by
+    // delta = [d == w1] - [c == w1] for the step-1 winner w1 (a constant per
+    // hypothesis, picked by step 1's mask), so the chain per step pair is
+    // sub -> sgn -> pick(delta) -> add -> sgn -> pick(inc) -> add instead of twice
+    // the single-step chain.
+    auto pair2 = [&](const uint4 &a1, const uint4 &b1, const uint4 &a2, const uint4 &b2, const uint4 &c2) {
+        const uint32_t va = prmt(L.lo, a1.x, L.hi), vb = prmt(L.lo, a1.y, L.hi);
+        const uint32_t vc = prmt(L.lo, a2.x, L.hi), vd = prmt(L.lo, a2.y, L.hi);
+        const uint32_t ga = b1.z & 0xffu, gb = (b1.z >> 8) & 0xffu, gc = b2.z & 0xffu, gd = (b2.z >> 8) & 0xffu;
+        const uint32_t m1 = sgn(vb - va);
+        const uint32_t m2 = sgn((vd - vc) + pick(c2.x, c2.y, m1));  // c2 = {dA, dA ^ dB} (pair_deltas)
+        L.lo += pick(a1.z, b1.x, m1) + pick(a2.z, b2.x, m2);
+        L.hi += pick(a1.w, b1.y, m1) + pick(a2.w, b2.y, m2);
+        s_choice[b1.w] = static_cast<int32_t>(pick(ga, ga ^ gb, m1));
+        s_choice[b2.w] = static_cast<int32_t>(pick(gc, gc ^ gd, m2));
+    };
     int s = 0;
     if (n2 >= 4) {
-        uint4 a[4], b[4];
+        uint4 a[4], b[4], c[2];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             a[i] = lds4(ent + i * kES);
             b[i] = lds4(ent + i * kES + 4);
         }
+        c[0] = lds4(ent + 1 * kES + 8);
+        c[1] = lds4(ent + 3 * kES + 8);
         for (; s + 4 <= n2; s += 4) {
-            uint4 an[4], bn[4];
+            uint4 an[4], bn[4], cn[2];
             const uint32_t *nx = ent + (s + 4) * kES;  // readable even past n2
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 an[i] = lds4(nx + i * kES);
                 bn[i] = lds4(nx + i * kES + 4);
             }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) step2(a[i], b[i]);
+            cn[0] = lds4(nx + 1 * kES + 8);
+            cn[1] = lds4(nx + 3 * kES + 8);
+            pair2(a[0], b[0], a[1], b[1], c[0]);
+            pair2(a[2], b[2], a[3], b[3], c[1]);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 a[i] = an[i];
                 b[i] = bn[i];
             }
+            c[0] = cn[0];
+            c[1] = cn[1];
         }
     }
     for (; s < n2; ++s) step2(lds4(ent + s * kES), lds4(ent + s * kES + 4));
@@ -595,7 +638,6 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
     const int32_t *s_part = reinterpret_cast<const int32_t *>(smem + L.part);
     uint64_t *s_keys = reinterpret_cast<uint64_t *>(smem + L.keys);
     int32_t *s_cand = reinterpret_cast<int32_t *>(smem + L.cand);
-    uint32_t *s_smask = reinterpret_cast<uint32_t *>(smem + L.smask);
     int32_t *s_sid = reinterpret_cast<int32_t *>(smem + L.sid);
     int32_t *s_L0 = reinterpret_cast<int32_t *>(smem + L.aux);
     uint32_t *s_ent = reinterpret_cast<uint32_t *>(smem + L.ent);
@@ -673,36 +715,55 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
         if (tid < 16) s_keys[m2 + tid] = ~0ull;  // pad for the paired scan
         __syncthreads();
         stamp(p, 4);
-        // ---- rank-by-count sort: four threads per candidate scan every 4th key
-        // pair with broadcast loads, quad shuffle-sum; the candidate's entries are
-        // written at slot = rank (packed layout for G <= 8, SoA masks always)
-        for (int c0 = 0; c0 < m2; c0 += kThreads / 4) {
-            const int c = c0 + (tid >> 2), part = tid & 3;
-            const uint64_t kc = (c < m2) ? s_keys[c] : 0ull;
-            // four independent counters: no compare -> add dependency chain
-            int r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+        // ---- rank-by-count sort.  Four warps per 32 candidates: lane = candidate,
+        // warp & 3 = a quarter of the key array.  Every lane of a warp reads the same
+        // key pair (a true broadcast: one shared-memory wavefront per load); the four
+        // quarter counts meet in shared memory.  Entries are written at slot = rank
+        // (packed layout for G <= 8, SoA masks always).
+        int32_t *s_rpart = reinterpret_cast<int32_t *>(smem + L.rpart);  // [4][N]
+        {
+            const int grp = warp >> 2, part = warp & 3;
+            for (int c0 = grp * 32; c0 < m2; c0 += (kWarps / 4) * 32) {
+                const int c = c0 + lane;
+                const uint64_t kc = (c < m2) ? s_keys[c] : 0ull;
+                int r0 = 0, r1 = 0, r2 = 0, r3 = 0;
 #pragma unroll 2
-            for (int c2 = 2 * part; c2 < m2; c2 += 16) {
-                const ulonglong2 k0 = *reinterpret_cast<const ulonglong2 *>(s_keys + c2);
-                const ulonglong2 k1 = *reinterpret_cast<const ulonglong2 *>(s_keys + c2 + 8);
-                r0 += k0.x < kc;
-                r1 += k0.y < kc;
-                r2 += k1.x < kc;
-                r3 += k1.y < kc;
+                for (int c2 = 2 * part; c2 < m2; c2 += 16) {
+                    const ulonglong2 k0 = *reinterpret_cast<const ulonglong2 *>(s_keys + c2);
+                    const ulonglong2 k1 = *reinterpret_cast<const ulonglong2 *>(s_keys + c2 + 8);
+                    r0 += k0.x < kc;
+                    r1 += k0.y < kc;
+                    r2 += k1.x < kc;
+                    r3 += k1.y < kc;
+                }
+                if (c < m2) s_rpart[part * N + c] = (r0 + r1) + (r2 + r3);
             }
-            int rk = (r0 + r1) + (r2 + r3);
-            rk += __shfl_xor_sync(kFull, rk, 1);
-            rk += __shfl_xor_sync(kFull, rk, 2);
-            if (c >= m2 || part != 0) continue;
-            if (c == 0) stamp(p, 13);
+        }
+        __syncthreads();
+        stamp(p, 13);
+        for (int c = tid; c < m2; c += kThreads) {
+            const int rk = (s_rpart[c] + s_rpart[N + c]) + (s_rpart[2 * N + c] + s_rpart[3 * N + c]);
             const int e = s_cand[c];
-            const int r = static_cast<int>(kc >> 56);
-#pragma unroll
-            for (int j = 0; j < W; ++j) s_smask[j * N + rk] = s_mask[e * W + j];
+            const int r = static_cast<int>(s_keys[c] >> 56);
             s_sid[rk] = e;
             if (try_packed) packed_entry(s_ent + rk * kES, r, s_mask[e], e);
             if (r == 2) atomicMax(&misc[M_N2], rk + 1);
             if (r <= 3) atomicMax(&misc[M_N3], rk + 1);  // end of the r=3 segment
+        }
+        if (try_packed) {
+            // step-pair corrections for the r=2 lookahead: for the pair (2j, 2j+1) with
+            // candidates (a, b) then (c, d), dX = [d == X] - [c == X]; stored in words 8..9
+            // of slot 2j+1 as {dA, dA ^ dB}
+            __syncthreads();
+            const int n2 = misc[M_N2];
+            for (int j = tid; 2 * j + 1 < n2; j += kThreads) {
+                const uint32_t g1 = s_ent[(2 * j) * kES + 6], g2 = s_ent[(2 * j + 1) * kES + 6];
+                const int ga = g1 & 0xff, gb = (g1 >> 8) & 0xff, gc = g2 & 0xff, gd = (g2 >> 8) & 0xff;
+                const uint32_t dA = static_cast<uint32_t>(static_cast<int>(gd == ga) - static_cast<int>(gc == ga));
+                const uint32_t dB = static_cast<uint32_t>(static_cast<int>(gd == gb) - static_cast<int>(gc == gb));
+                s_ent[(2 * j + 1) * kES + 8] = dA;
+                s_ent[(2 * j + 1) * kES + 9] = dA ^ dB;
+            }
         }
     } else {
         // caller-supplied order (metro-parallel): single-replica experts included
@@ -712,11 +773,7 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
             int r = 0;
             if (e >= 0 && e < N) {
 #pragma unroll
-                for (int j = 0; j < W; ++j) {
-                    const uint32_t w = s_mask[e * W + j];
-                    s_smask[j * N + s] = w;
-                    r += __popc(w);
-                }
+                for (int j = 0; j < W; ++j) r += __popc(s_mask[e * W + j]);
                 s_sid[s] = e;
             }
             if (e < 0 || e >= N || r == 0) atomicMin(&misc[M_NOREP], (e < 0 || e >= N) ? -1 : e);
@@ -768,6 +825,10 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
         }
         __syncthreads();
         done = misc[M_PACKED_OK] != 0;
+        if (done) {
+            stamp(p, 6);
+            return true;
+        }
     }
     if (!done) {
         // ---- serial greedy (routing.py:94-101) in warp 0, any G <= 128.
@@ -784,12 +845,13 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
                 Lk[k] = (g < G) ? ((static_cast<uint32_t>(s_L0[g]) << 8) | static_cast<uint32_t>(g)) : 0xffffffffu;
             }
             for (int base = 0; base < m2; base += 32) {
-                const int j = base + lane;
+                    const int j = base + lane;
                 const bool v = j < m2;
+                const int myid = v ? s_sid[j] : 0;
                 uint32_t cb[W];
 #pragma unroll
                 for (int k = 0; k < W; ++k) {
-                    const uint32_t m = v ? s_smask[k * N + j] : 0u;
+                    const uint32_t m = v ? s_mask[myid * W + k] : 0u;
                     cb[k] = 0;
                     const int gk = min(32, G - 32 * k);
                     for (int b = 0; b < gk; ++b) {
@@ -797,7 +859,6 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
                         if (lane == b) cb[k] = bb;
                     }
                 }
-                const int myid = v ? s_sid[j] : 0;
                 const int steps = min(32, m2 - base);
                 uint32_t wmine = 0;
 #pragma unroll
@@ -833,17 +894,17 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
 }
 
 // ================================================================ kernels
-template <int W>
+template <int W, bool PRIV>
 __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t R = cluster_nctarank(), rank = cluster_ctarank();
-    if (R > 1) cluster_arrive_relaxed();  // paired with the wait before the first DSMEM store
-    const Layout L = make_layout(kMetroIds, p.N, W, R, p.slice, p.C, p.staged);
+    const Layout L = make_layout(kMetroIds, p.N, W, R, p.slice, p.C, p.staged, PRIV);
     const int64_t beg = static_cast<int64_t>(rank) * p.slice;
     const int64_t rem_pairs = p.num_pairs - beg;
     const int n_local = rem_pairs <= 0 ? 0 : static_cast<int>(rem_pairs < p.slice ? rem_pairs : p.slice);
     const StagePlan sp = stage_plan<W>(p, beg, n_local, p.staged != 0);
     if (threadIdx.x == 0) stage_issue(p, L, smem, beg, sp);
+    if (R > 1) cluster_arrive_release();  // after thread 0 initialised the mbarriers
     stamp(p, 0);
     int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
     init_misc(misc);
@@ -852,7 +913,7 @@ __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) 
     __syncthreads();
     mbar_wait(reinterpret_cast<uint64_t *>(smem + L.mbar), 0);
     stamp(p, 1);
-    histogram_push<false>(p, L, smem, beg, n_local, R, rank);
+    histogram_push<PRIV>(p, L, smem, beg, n_local, R, rank);
     const bool writer = (rank == 0);
     if (!p.mask) {  // aggregate_loads only (core.py:236-244)
         bad_min_warp0(L, smem, R, p.N);
@@ -884,14 +945,26 @@ __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) 
         const bool vec = ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) &&
                          (p.staged || ((reinterpret_cast<uintptr_t>(src) & 15) == 0));
         if (vec) {
-            for (int i = threadIdx.x * 4; i < n4; i += kThreads * 4) {
-                const int4 v = *reinterpret_cast<const int4 *>(src + i);
-                int4 o;
-                o.x = s_choice[v.x];
-                o.y = s_choice[v.y];
-                o.z = s_choice[v.z];
-                o.w = s_choice[v.w];
-                *reinterpret_cast<int4 *>(dst + i) = o;
+            // four 16-byte groups per thread per round: all id loads, then all choice
+            // gathers, then the stores (one latency round instead of four)
+            constexpr int U = 4;
+            for (int i0 = threadIdx.x * 4; i0 < n4; i0 += kThreads * 4 * U) {
+                int4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + u * kThreads * 4;
+                    v[u] = (i < n4) ? *reinterpret_cast<const int4 *>(src + i) : make_int4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = i0 + u * kThreads * 4;
+                    int4 o;
+                    o.x = s_choice[v[u].x];
+                    o.y = s_choice[v[u].y];
+                    o.z = s_choice[v[u].z];
+                    o.w = s_choice[v[u].w];
+                    if (i < n4) *reinterpret_cast<int4 *>(dst + i) = o;
+                }
             }
         }
         for (int i = (vec ? n4 : 0) + threadIdx.x; i < n_local; i += kThreads) dst[i] = s_choice[src[i]];
@@ -1035,13 +1108,13 @@ template <int W, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) eplb_ids_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t R = cluster_nctarank(), rank = cluster_ctarank();
-    if (R > 1) cluster_arrive_relaxed();
     const Layout L = make_layout(kEplbIds, p.N, W, R, p.slice, p.C, p.staged, PAIR);
     const int64_t beg = static_cast<int64_t>(rank) * p.slice;
     const int64_t rem_pairs = p.num_pairs - beg;
     const int n_local = rem_pairs <= 0 ? 0 : static_cast<int>(rem_pairs < p.slice ? rem_pairs : p.slice);
     const StagePlan sp = stage_plan<W>(p, beg, n_local, p.staged != 0);
     if (threadIdx.x == 0) stage_issue(p, L, smem, beg, sp);
+    if (R > 1) cluster_arrive_release();  // after thread 0 initialised the mbarriers
     int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
     init_misc(misc);
     zero_smem(smem, L.aux, L.part);  // rank counts + histogram
@@ -1201,6 +1274,16 @@ static int copies_for(int N) {
     while (C > 1 && N * C * 4 > 64 * 1024) C >>= 1;
     return C;
 }
+// METRO histogram strategy: 1 = lane-striped shared atomics (default; measured
+// 7x faster on B200 than 0 = warp-private match_any + plain RMW, which stays
+// selectable with METRO_HIST=match for tuning)
+static int hist_mode() {
+    static const int mode = [] {
+        const char *v = getenv("METRO_HIST");
+        return (v && strcmp(v, "match") == 0) ? 0 : 1;
+    }();
+    return mode;
+}
 static int auto_cluster(int64_t num_pairs) {
     int R = 1;
     while (R < kMaxCluster && num_pairs > (int64_t)R * 1024) R <<= 1;
@@ -1311,10 +1394,20 @@ int metro_route_v1(const int32_t *ids, int64_t num_pairs, const uint32_t *mask, 
     p.loads = loads; p.choice = choice; p.rank_counts = rank_counts; p.lam = lam;
     p.pair_rank = pair_rank; p.status = status; p.stamps = g_stamps;
     int R = 1;
-    const int smem = plan_ids(kMetroIds, false, num_pairs, N, W, cluster_ctas, p, R);
+    // warp-private histograms (match_any + plain RMW, no shared atomics) when they fit
+    bool priv = hist_mode() != 1;
+    int smem = priv ? plan_ids(kMetroIds, true, num_pairs, N, W, cluster_ctas, p, R) : METRO_EDIMS;
+    if (smem < 0) {
+        priv = false;
+        smem = plan_ids(kMetroIds, false, num_pairs, N, W, cluster_ctas, p, R);
+    }
     if (smem < 0) return smem;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    METRO_DISPATCH_W(W, return launch(metro_ids_kernel<kW>, R, smem, s, p));
+    if (priv) {
+        METRO_DISPATCH_W(W, return launch(metro_ids_kernel<kW, true>, R, smem, s, p));
+    } else {
+        METRO_DISPATCH_W(W, return launch(metro_ids_kernel<kW, false>, R, smem, s, p));
+    }
     return METRO_EDIMS;
 }
 
@@ -1328,7 +1421,7 @@ int metro_aggregate_loads_v1(const int32_t *ids, int64_t num_pairs, int32_t N, i
     int R = 1;
     const int smem = plan_ids(kMetroIds, false, num_pairs, N, 1, cluster_ctas, p, R);
     if (smem < 0) return smem;
-    return launch(metro_ids_kernel<1>, R, smem, static_cast<cudaStream_t>(stream), p);
+    return launch(metro_ids_kernel<1, false>, R, smem, static_cast<cudaStream_t>(stream), p);
 }
 
 int metro_route_from_loads_v1(const int64_t *loads, const uint32_t *mask, int32_t N, int32_t G,

@@ -56,10 +56,11 @@ def build_items(groups: Sequence[Tuple[int, int, int]], M: int) -> np.ndarray:
         raise ValidationError(f"M={M} must be a multiple of {BM}")
     out = []
     for e, t0, n in groups:
-        for c0 in range(0, n, MAXN):
-            nn = min(MAXN, n - c0)
-            for mb in range(M // BM):
-                out.append((e, mb, t0 + c0, nn))
+        # token chunks of one weight block are adjacent, so the CTAs that run them
+        # concurrently share the block's HBM read through L2
+        for mb in range(M // BM):
+            for c0 in range(0, n, MAXN):
+                out.append((e, mb, t0 + c0, min(MAXN, n - c0)))
     return np.asarray(out, dtype=np.int32).reshape(-1, 4)
 
 

@@ -60,7 +60,9 @@ def main():
                           "r2": int(s[8] - s[5]), "r3": int(s[9] - s[8]), "rgen": int(s[10] - s[9]),
                           "greedy_tail": int(s[6] - s[10]),
                           "c_head": int(s[14] - s[3]), "c_body": int(s[17] - s[14]),
-                          "c_tail": int(s[11] - s[17])}
+                          "c_tail": int(s[11] - s[17]),
+                          "x_entrywait": int(s[20] - s[2]), "x_sums_push": int(s[18] - s[20]),
+                          "x_arrive": int(s[19] - s[18]), "x_wait": int(s[3] - s[19])}
             # back-to-back graph replay over a pool of distinct batches > L2
             per = ids.numel() * 4
             P = max(64, (256 << 20) // per)
