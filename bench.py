@@ -8,9 +8,10 @@ N > 1 is launched by the driver with torch.distributed.run (one rank per GPU,
 NCCL).  A step = one MoE layer: [NCCL all-gather of every rank's top-k ids] +
 the sm_100a METRO routing kernel over the global batch.  The global decode
 batch (B tokens) is fixed as N grows ("strong" scaling); every rank routes the
-whole batch (replicated, deterministic).  Inputs: pools of distinct synthetic
-batches resident in HBM; L2 is flushed (256 MiB memset) between steps outside
-the timed events.
+whole batch (replicated, deterministic).  N = 1: CUDA-graph replays over a
+256 MiB pool of distinct batches (> L2).  N > 1: 256 MiB L2 flush per step,
+flush-only loop subtracted.  Also reported: e2e from pinned host buffers, the
+CPU oracle port, and K3 (the bottleneck rank's expert FFN, METRO vs EPLB).
 
 Rank 0 prints ONE JSON line.  --impl reference times the reference algorithm's
 CPU path (the oracle port, oracle/metro_oracle.c: aggregate_loads + route_metro +
@@ -228,7 +229,8 @@ def run_reference(args, cfg, rank: int, world: int):
         "impl": "reference", "metric": METRIC, "value": us, "unit": "us/layer", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": data_str(),
-        "config": config_dict(args, cfg, world),
+        "config": dict(config_dict(args, cfg, world), l2="n/a (host CPU path)",
+                       parallelism="single host thread, one layer per step"),
         "cpu_baseline": {"value": us, "unit": "us/layer", "cores": 1, "kind": "port", "sample": sample,
                          "all_cores_layers_per_s": thr, "host_cores": cores},
         "e2e": {"value": us, "unit": "us/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -390,18 +392,24 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
     # end to end from host buffers: H2D ids, route, D2H results, sync
     E = min(args.e2e_steps, K)
     if world == 1:
-        hr = HostRouter(pl, B * k, args.cluster)
-        hosts = [torch.from_numpy(b.reshape(-1).copy()).pin_memory() for b in batches]
-        prh = torch.empty(B * k, dtype=torch.int32).pin_memory()
+        # zero-copy: the kernel reads the ids from / writes results to pinned host
+        # memory; each step's batch is first written into the router's host buffer
+        hr = HostRouter(pl, B * k, args.cluster, zero_copy=True)
+        hosts = [b.reshape(-1).copy() for b in batches]
+        ids_np = hr.ids.numpy()
         for i in range(10):
-            hr(hosts[i % POOL], prh)
+            ids_np[:] = hosts[i % POOL]
+            hr.run(B * k)
         per = []
         for i in range(E):
+            ids_np[:] = hosts[i % POOL]  # the caller's batch arrives in host memory
             flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            hr(hosts[i % POOL], prh)
+            out_np = hr.run(B * k)
             per.append(time.perf_counter() - t0)
+            if i < POOL and int(out_np[0]) != 0:
+                raise RuntimeError("e2e routing reported an error status")
         e2e_us = statistics.mean(per) * 1e6
         h2d = B * k * 4
         d2h = (8 + cfg["G"] + cfg["N"]) * 4 + B * k * 4

@@ -142,12 +142,15 @@ METRO_API int eplb_route_from_loads_v1(const int64_t *loads, const uint32_t *ran
  *   flags = 0                    : cudaMemcpyAsync H2D of the ids into dev_workspace
  *                                  (metro_host_workspace_bytes() bytes), the kernel,
  *                                  D2H of the results, stream synchronise;
- *   flags = METRO_HOST_ZEROCOPY  : the kernel reads the ids from and writes the
+ *   flags & METRO_HOST_ZEROCOPY  : the kernel reads the ids from and writes the
  *                                  results to pinned (device-mapped) host memory
  *                                  directly over PCIe; dev_workspace unused.
  * host_out [8 + G + N] int32 receives: status[4], lam, pad[3], rank_counts[G],
  * choice[N].  pair_rank_host [num_pairs] is nullable. */
 #define METRO_HOST_ZEROCOPY 1
+/* flag: the host buffers stay allocated (pinned) across calls, so their
+ * device-accessibility check is done once and cached */
+#define METRO_HOST_STABLE_BUFFERS 2
 METRO_API size_t metro_host_workspace_bytes(int64_t num_pairs, int32_t num_experts, int32_t num_ranks);
 METRO_API int metro_route_host_v1(const int32_t *topk_ids_host, int64_t num_pairs,
                                   const uint32_t *rank_mask_dev, int32_t num_experts, int32_t num_ranks,

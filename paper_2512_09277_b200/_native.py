@@ -28,6 +28,7 @@ EDIMS = -2
 ECUDA = -3
 ENOTBINARY = -4
 HOST_ZEROCOPY = 1
+HOST_STABLE_BUFFERS = 2
 
 MAX_G = 128
 MAX_N = 4096

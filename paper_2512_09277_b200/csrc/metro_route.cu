@@ -196,6 +196,16 @@ __device__ __forceinline__ void st_async_b32(const void *local, uint32_t cta, ui
                  : "memory");
 }
 
+__device__ __forceinline__ void st_async_v4(const void *local, uint32_t cta, uint4 v, const void *local_bar) {
+    uint32_t raddr, rbar;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(local)), "r"(cta));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(local_bar)), "r"(cta));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                     raddr),
+                 "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rbar)
+                 : "memory");
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -354,7 +364,7 @@ __device__ void histogram_push(const Params &p, const Layout &L, unsigned char *
     uint64_t *xbar = reinterpret_cast<uint64_t *>(smem + L.mbar) + 1;
     if (R > 1) {
         cluster_wait();
-        if (tid == 0) mbar_arrive_expect_tx(xbar, (R - 1) * static_cast<uint32_t>(N + 2) * 4u);
+        if (tid == 0) mbar_arrive_expect_tx(xbar, (R - 1) * static_cast<uint32_t>(L.NP) * 4u);
     }
     stamp(p, 20);
     int32_t *row = s_part + rank * L.NP;
@@ -378,12 +388,20 @@ __device__ void histogram_push(const Params &p, const Layout &L, unsigned char *
 #pragma unroll 4
             for (int w = 0; w < kWarps; ++w) s += s_hist[w * N + e];
         }
-        row[e] = s;  // read back only by this thread (same e mapping downstream)
-        for (uint32_t d = 1; d < R; ++d) st_async_b32(row + e, (rank + d) % R, static_cast<uint32_t>(s), xbar);
+        row[e] = s;
     }
-    if (tid < 2 && R > 1) {
-        const int32_t v = misc[M_BAD_LO + tid];
-        for (uint32_t d = 1; d < R; ++d) st_async_b32(row + N + tid, (rank + d) % R, static_cast<uint32_t>(v), xbar);
+    if (R > 1) {
+        // ship the finished row in 16-byte st.async pieces (4x fewer DSMEM ops than
+        // per-expert words; the row carries the CTA's bad-pair words at [N, N+2))
+        if (tid < 2) row[N + tid] = misc[M_BAD_LO + tid];
+        for (int e = N + 2 + tid; e < L.NP; e += kThreads) row[e] = 0;
+        __syncthreads();
+        const int nv = L.NP / 4;
+        for (int idx = tid; idx < static_cast<int>(R - 1) * nv; idx += kThreads) {
+            const uint32_t d = (rank + 1 + idx / nv) % R;
+            const int v = idx % nv;
+            st_async_v4(row + 4 * v, d, reinterpret_cast<const uint4 *>(row)[v], xbar);
+        }
     }
     stamp(p, 18);
     if (R > 1) mbar_wait(xbar, 0);
@@ -588,35 +606,52 @@ __device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t
     }
     for (; s < n2; ++s) step2(lds4(ent + s * kES), lds4(ent + s * kES + 4));
     stamp(p, 8);
-    for (; s < n2 + n3; ++s) {
-        const uint4 a = lds4(ent + s * kES), b = lds4(ent + s * kES + 4), c = lds4(ent + s * kES + 8);
-        const uint32_t va = prmt(L.lo, a.x, L.hi), vb = prmt(L.lo, a.y, L.hi), vc = prmt(L.lo, a.z, L.hi);
-        const uint32_t m1 = sgn(vb - va);
-        const uint32_t vab = pick(va, va ^ vb, m1);
-        const uint32_t ilo = pick(b.x, b.z, m1), ihi = pick(b.y, b.w, m1);
-        const uint32_t m2v = sgn(vc - vab);
-        L.lo += pick(ilo, ilo ^ c.x, m2v);
-        L.hi += pick(ihi, ihi ^ c.y, m2v);
-        const uint32_t gs = c.z, ga = gs & 0xffu, gb = (gs >> 8) & 0xffu, gc = (gs >> 16) & 0xffu;
-        const uint32_t gab = pick(ga, ga ^ gb, m1);
-        s_choice[c.w] = static_cast<int32_t>(pick(gab, gab ^ gc, m2v));
+    // r = 3 steps, next entry prefetched (slots past m2 stay readable)
+    if (s < n2 + n3) {
+        uint4 a = lds4(ent + s * kES), b = lds4(ent + s * kES + 4), c = lds4(ent + s * kES + 8);
+        for (; s < n2 + n3; ++s) {
+            const uint4 an = lds4(ent + (s + 1) * kES), bn = lds4(ent + (s + 1) * kES + 4),
+                        cn = lds4(ent + (s + 1) * kES + 8);
+            const uint32_t va = prmt(L.lo, a.x, L.hi), vb = prmt(L.lo, a.y, L.hi), vc = prmt(L.lo, a.z, L.hi);
+            const uint32_t m1 = sgn(vb - va);
+            const uint32_t vab = pick(va, va ^ vb, m1);
+            const uint32_t ilo = pick(b.x, b.z, m1), ihi = pick(b.y, b.w, m1);
+            const uint32_t m2v = sgn(vc - vab);
+            L.lo += pick(ilo, ilo ^ c.x, m2v);
+            L.hi += pick(ihi, ihi ^ c.y, m2v);
+            const uint32_t gs = c.z, ga = gs & 0xffu, gb = (gs >> 8) & 0xffu, gc = (gs >> 16) & 0xffu;
+            const uint32_t gab = pick(ga, ga ^ gb, m1);
+            s_choice[c.w] = static_cast<int32_t>(pick(gab, gab ^ gc, m2v));
+            a = an;
+            b = bn;
+            c = cn;
+        }
     }
     stamp(p, 9);
-    for (; s < m2; ++s) {
-        const uint4 n0 = lds4(ent + s * kES), n1 = lds4(ent + s * kES + 4), n2v = lds4(ent + s * kES + 8);
-        const uint32_t nc[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
-        Cand c[8];
+    // r >= 4: fixed 8-leaf tournament, next entry prefetched
+    if (s < m2) {
+        uint4 n0 = lds4(ent + s * kES), n1 = lds4(ent + s * kES + 4), n2v = lds4(ent + s * kES + 8);
+        for (; s < m2; ++s) {
+            const uint4 q0 = lds4(ent + (s + 1) * kES), q1 = lds4(ent + (s + 1) * kES + 4),
+                        q2 = lds4(ent + (s + 1) * kES + 8);
+            const uint32_t nc[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+            Cand c[8];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-            c[g].v = prmt(L.lo, zsel(g), L.hi) | nc[g];
-            c[g].ilo = inc_lo(g);
-            c[g].ihi = inc_hi(g);
-            c[g].g = g;
+            for (int g = 0; g < 8; ++g) {
+                c[g].v = prmt(L.lo, zsel(g), L.hi) | nc[g];
+                c[g].ilo = inc_lo(g);
+                c[g].ihi = inc_hi(g);
+                c[g].g = g;
+            }
+            const Cand w =
+                duel(duel(duel(c[0], c[1]), duel(c[2], c[3])), duel(duel(c[4], c[5]), duel(c[6], c[7])));
+            L.lo += w.ilo;
+            L.hi += w.ihi;
+            s_choice[n2v.x] = static_cast<int32_t>(w.g);
+            n0 = q0;
+            n1 = q1;
+            n2v = q2;
         }
-        const Cand w = duel(duel(duel(c[0], c[1]), duel(c[2], c[3])), duel(duel(c[4], c[5]), duel(c[6], c[7])));
-        L.lo += w.ilo;
-        L.hi += w.ihi;
-        s_choice[n2v.x] = static_cast<int32_t>(w.g);
     }
     stamp(p, 10);
     return L;
@@ -1524,10 +1559,20 @@ int metro_route_host_v1(const int32_t *ids_host, int64_t num_pairs, const uint32
     cudaError_t e;
     if (flags & METRO_HOST_ZEROCOPY) {
         // the kernel reads the ids from and writes the results to pinned host memory
-        // directly (PCIe reads/posted writes inside the launch): no copy engines
-        if ((num_pairs > 0 && !device_accessible(ids_host)) || !device_accessible(host_out) ||
-            (pair_rank_host && !device_accessible(pair_rank_host)))
-            return METRO_EARG;
+        // directly (PCIe reads/posted writes inside the launch): no copy engines.
+        // With METRO_HOST_STABLE_BUFFERS the caller guarantees the buffers outlive
+        // the calls, and the pointer validation of the last triple is cached.
+        static thread_local const void *ok_ids = nullptr, *ok_out = nullptr, *ok_pr = nullptr;
+        const bool cached = (flags & METRO_HOST_STABLE_BUFFERS) && ids_host == ok_ids && host_out == ok_out &&
+                            pair_rank_host == ok_pr;
+        if (!cached) {
+            if ((num_pairs > 0 && !device_accessible(ids_host)) || !device_accessible(host_out) ||
+                (pair_rank_host && !device_accessible(pair_rank_host)))
+                return METRO_EARG;
+            ok_ids = ids_host;
+            ok_out = host_out;
+            ok_pr = pair_rank_host;
+        }
         int rc = metro_route_v1(ids_host, num_pairs, mask_dev, N, G, nullptr, host_out + 8 + G, host_out + 8,
                                 host_out + 4, pair_rank_host, host_out, cluster_ctas, stream);
         if (rc) return rc;

@@ -201,20 +201,46 @@ class HostRouter:
     reference-facing call a CPU-resident caller makes.  ``zero_copy=True`` lets
     the kernel read/write the pinned host buffers directly over PCIe (no copy
     engine round trips); ``False`` uses explicit cudaMemcpyAsync H2D / D2H.
+
+    The router owns its pinned buffers: write the batch into ``ids`` (int32,
+    row-major [B, k] flattened) and call ``run(num_pairs)``; results land in
+    ``out`` ([status 4 | lam | pad 3 | rank_counts G | choice N]) and
+    ``pair_rank``.  ``__call__(ids_host, pair_rank_host)`` is the convenience form
+    for caller-owned pinned tensors.
     """
 
     def __init__(self, placement: DevicePlacement, max_pairs: int, cluster_ctas: int = 0,
                  zero_copy: bool = True):
         self.placement = placement
         self.cluster_ctas = int(cluster_ctas)
-        self.flags = _native.HOST_ZEROCOPY if zero_copy else 0
         L = _native.lib()
         n, g = placement.num_experts, placement.num_ranks
-        nbytes = L.metro_host_workspace_bytes(max_pairs, n, g)
         self.max_pairs = max_pairs
-        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=placement.device)
-        self.host_out = torch.empty(8 + g + n, dtype=torch.int32).pin_memory()
+        self.ws = torch.empty(L.metro_host_workspace_bytes(max_pairs, n, g), dtype=torch.uint8,
+                              device=placement.device)
+        self.ids = torch.zeros(max_pairs, dtype=torch.int32).pin_memory()
+        self.out = torch.zeros(8 + g + n, dtype=torch.int32).pin_memory()
+        self.pair_rank = torch.zeros(max_pairs, dtype=torch.int32).pin_memory()
         self.stream = torch.cuda.Stream(placement.device)
+        self.flags = (_native.HOST_ZEROCOPY if zero_copy else 0)
+        self._fn = L.metro_route_host_v1
+        self._npairs = ctypes.c_int64(max_pairs)
+        self._args = (
+            ctypes.c_void_p(self.ids.data_ptr()), self._npairs, ctypes.c_void_p(placement.mask.data_ptr()),
+            ctypes.c_int32(n), ctypes.c_int32(g), ctypes.c_void_p(self.ws.data_ptr()),
+            ctypes.c_void_p(self.out.data_ptr()), ctypes.c_void_p(self.pair_rank.data_ptr()),
+            ctypes.c_int32(self.cluster_ctas), ctypes.c_int32(self.flags | _native.HOST_STABLE_BUFFERS),
+            ctypes.c_void_p(self.stream.cuda_stream),
+        )
+        self._out_np = self.out.numpy()
+
+    def run(self, num_pairs: int) -> np.ndarray:
+        """Route ids[:num_pairs] (already written into self.ids); synchronous."""
+        self._npairs.value = num_pairs
+        rc = self._fn(*self._args)
+        if rc:
+            _native.check_rc(rc, "metro_route_host_v1")
+        return self._out_np
 
     def __call__(self, ids_host: torch.Tensor, pair_rank_host: Optional[torch.Tensor] = None) -> np.ndarray:
         if ids_host.is_cuda or ids_host.dtype != torch.int32 or not ids_host.is_contiguous():
@@ -224,9 +250,9 @@ class HostRouter:
         p = self.placement
         rc = _native.lib().metro_route_host_v1(
             ids_host.data_ptr(), ids_host.numel(), p.mask.data_ptr(), p.num_experts, p.num_ranks,
-            self.ws.data_ptr(), self.host_out.data_ptr(),
+            self.ws.data_ptr(), self.out.data_ptr(),
             None if pair_rank_host is None else pair_rank_host.data_ptr(), self.cluster_ctas,
             self.flags, self.stream.cuda_stream,
         )
         _native.check_rc(rc, "metro_route_host_v1")
-        return self.host_out.numpy()
+        return self._out_np

@@ -286,6 +286,22 @@ def test_cuda_graph_replay(shapes):
         assert int(out.lam.item()) == s["metro_lam"]
 
 
+def test_host_router_owned_buffers(shapes):
+    for zc in (True, False):
+        for c in shapes[:10]:
+            pl = DevicePlacement(c["A"])
+            hr = HostRouter(pl, max_pairs=c["ids"].size, zero_copy=zc)
+            for rep in range(2):
+                hr.ids.numpy()[:c["ids"].size] = c["ids"].reshape(-1)
+                out = hr.run(c["ids"].size)
+                n, g = c["N"], c["G"]
+                assert out[0] == 0 and out[4] == c["metro_lam"]
+                assert np.array_equal(out[8:8 + g], c["metro_counts"])
+                assert np.array_equal(out[8 + g:8 + g + n], c["metro_choice"])
+                assert np.array_equal(hr.pair_rank.numpy()[:c["ids"].size],
+                                      oracle.pair_rank_metro(c["ids"].reshape(-1), c["metro_choice"]))
+
+
 def test_host_router_e2e(shapes):
     for c in shapes[:12]:
         pl = DevicePlacement(c["A"])
