@@ -44,6 +44,16 @@ from .routing import (
     save_assignment,
 )
 from .device import DevicePlacement, HostRouter, RouteResult, Router, pack_placement
+from .io import (
+    Trace,
+    TraceBatch,
+    TraceFormatError,
+    load_placement,
+    load_trace,
+    load_trace_topk,
+    save_placement,
+    save_trace,
+)
 from ._native import NativeLibraryError
 
 __all__ = [
@@ -54,7 +64,8 @@ __all__ = [
     "route_eplb", "route_metro", "route_metro_parallel", "route_optimal", "run_router",
     "save_assignment", "validate_assignment", "zipf_popularity",
     "DevicePlacement", "HostRouter", "RouteResult", "Router", "pack_placement",
-    "NativeLibraryError",
+    "NativeLibraryError", "Trace", "TraceBatch", "TraceFormatError", "load_placement", "load_trace",
+    "load_trace_topk", "save_placement", "save_trace",
 ]
 
 __version__ = "0.1.0"

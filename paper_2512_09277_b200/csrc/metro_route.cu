@@ -115,7 +115,7 @@ __host__ __device__ inline Layout make_layout(int kind, int N, int W, int R, int
     L.ent = align_up(L.sid + N * 4, 16);
     // packed-greedy entries (W == 1 only), one slot per rank + readable padding
     L.rpart = align_up(L.ent + (W == 1 ? (N + 16) * kES * 4 : 0), 16);  // [4][N] partial ranks
-    const int end2 = metro ? align_up(L.rpart + 4 * N * 4, 16) : o;
+    const int end2 = metro ? align_up(L.rpart + (4 * N + 16) * 4, 16) : o;  // + prefetch slack
     L.total = end1 > end2 ? end1 : end2;
     return L;
 }
@@ -482,6 +482,16 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t sel, uint32_t b) {
 __host__ __device__ constexpr uint32_t zsel(uint32_t g) {
     return g | ((8u | g) << 4) | ((8u | g) << 8) | ((8u | g) << 12);
 }
+// byte g of {lo, hi} moved to byte 1, other bytes zero (sign-fill of a byte < 128)
+__host__ __device__ constexpr uint32_t zsel1(uint32_t g) {
+    return (8u | g) | (g << 4) | ((8u | g) << 8) | ((8u | g) << 12);
+}
+// PTX shl clamps shift amounts >= 32 to 32 (result 0); unsigned wrap of sh - 32 included
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t v, uint32_t sh) {
+    uint32_t d;
+    asm("shl.b32 %0, %1, %2;" : "=r"(d) : "r"(v), "r"(sh));
+    return d;
+}
 __device__ __forceinline__ uint32_t sgn(uint32_t d) { return prmt(d, 0xBBBBu, 0u); }  // 0 or ~0
 __device__ __forceinline__ uint32_t pick(uint32_t a, uint32_t x, uint32_t m) {
     uint32_t d;  // a ^ (x & m)
@@ -502,7 +512,7 @@ __host__ __device__ constexpr uint32_t inc_hi(uint32_t g) { return g >= 4 ? (1u 
 //   r=2  {selA, selB, incA_lo, incA_hi, xAB_lo, xAB_hi, ga | gb << 8, id}
 //   r=3  {selA, selB, selC, 0, incA_lo, incA_hi, xAB_lo, xAB_hi, incC_lo, incC_hi,
 //         ga | gb << 8 | gc << 16, id}
-//   r>=4 {nc0..nc7 (127 for non-candidates, else 0), id, 0, 0, 0}
+//   r>=4 {c0..c7 (8g, + 0x7f00 for non-candidates), id, 0, 0, 0}
 __device__ __forceinline__ void packed_entry(uint32_t *dst, int r, uint32_t m, int e) {
     if (r == 2 || r == 3) {
         const uint32_t m1 = m & (m - 1), m2 = m1 & (m1 - 1);
@@ -519,92 +529,102 @@ __device__ __forceinline__ void packed_entry(uint32_t *dst, int r, uint32_t m, i
                 make_uint4(inc_lo(g[2]), inc_hi(g[2]), g[0] | (g[1] << 8) | (g[2] << 16), static_cast<uint32_t>(e));
         }
     } else {
+        // key offsets: 8g in the low byte (tie-break on the lower rank id, and the
+        // increment's shift); non-candidates pushed above every valid counter
         uint32_t nc[8];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) nc[g] = ((m >> g) & 1u) ? 0u : 127u;
+        for (int g = 0; g < 8; ++g) nc[g] = (((m >> g) & 1u) ? 0u : 0x7f00u) | (8u * g);
         reinterpret_cast<uint4 *>(dst)[0] = make_uint4(nc[0], nc[1], nc[2], nc[3]);
         reinterpret_cast<uint4 *>(dst)[1] = make_uint4(nc[4], nc[5], nc[6], nc[7]);
         reinterpret_cast<uint4 *>(dst)[2] = make_uint4(static_cast<uint32_t>(e), 0u, 0u, 0u);
     }
 }
 
-// one tournament node: right wins only on strictly smaller value
-struct Cand {
-    uint32_t v, ilo, ihi, g;
-};
-__device__ __forceinline__ Cand duel(const Cand &l, const Cand &r) {
-    const uint32_t m = sgn(r.v - l.v);
-    Cand o;
-    o.v = pick(l.v, l.v ^ r.v, m);
-    o.ilo = pick(l.ilo, l.ilo ^ r.ilo, m);
-    o.ihi = pick(l.ihi, l.ihi ^ r.ihi, m);
-    o.g = pick(l.g, l.g ^ r.g, m);
-    return o;
-}
-
 // One thread.  Entries live at slot = rank (stride kES words) and are grouped
 // by r because the canonical order sorts by r first: [0, n2) r=2,
 // [n2, n2 + n3) r=3, [n2 + n3, m2) r>=4.  Slots up to m2 + 8 are readable (the
 // r=2 prefetch may touch them; they are never applied).
-__device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t *ent, int n2, int n3, int m2,
-                                                 int32_t *s_choice, PackedL L) {
+__device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t *ent, const uint32_t *dlt, int n2,
+                                                 int n3, int m2, uint8_t *dec, PackedL L) {
+    uint8_t dec_s = 0;
     auto step2 = [&](const uint4 &a, const uint4 &b) {
         const uint32_t va = prmt(L.lo, a.x, L.hi), vb = prmt(L.lo, a.y, L.hi);
         const uint32_t m = sgn(vb - va);
         L.lo += pick(a.z, b.x, m);
         L.hi += pick(a.w, b.y, m);
-        const uint32_t gs = b.z;
-        s_choice[b.w] = static_cast<int32_t>(pick(gs & 0xffu, (gs ^ (gs >> 8)) & 0xffu, m));
+        dec_s = static_cast<uint8_t>(m);  // decision only: choices are written in parallel later
     };
-    // Two consecutive r=2 steps (a, b) then (c, d) in one dependency chain: all four
-    // loads are extracted from the same L, and step 2 corrects its difference by
-    // delta = [d == w1] - [c == w1] for the step-1 winner w1 (a constant per
-    // hypothesis, picked by step 1's mask), so the chain per step pair is
-    // sub -> sgn -> pick(delta) -> add -> sgn -> pick(inc) -> add instead of twice
-    // the single-step chain.
-    auto pair2 = [&](const uint4 &a1, const uint4 &b1, const uint4 &a2, const uint4 &b2, const uint4 &c2) {
-        const uint32_t va = prmt(L.lo, a1.x, L.hi), vb = prmt(L.lo, a1.y, L.hi);
-        const uint32_t vc = prmt(L.lo, a2.x, L.hi), vd = prmt(L.lo, a2.y, L.hi);
-        const uint32_t ga = b1.z & 0xffu, gb = (b1.z >> 8) & 0xffu, gc = b2.z & 0xffu, gd = (b2.z >> 8) & 0xffu;
-        const uint32_t m1 = sgn(vb - va);
-        const uint32_t m2 = sgn((vd - vc) + pick(c2.x, c2.y, m1));  // c2 = {dA, dA ^ dB} (pair_deltas)
-        L.lo += pick(a1.z, b1.x, m1) + pick(a2.z, b2.x, m2);
-        L.hi += pick(a1.w, b1.y, m1) + pick(a2.w, b2.y, m2);
-        s_choice[b1.w] = static_cast<int32_t>(pick(ga, ga ^ gb, m1));
-        s_choice[b2.w] = static_cast<int32_t>(pick(gc, gc ^ gd, m2));
+    // Four consecutive r=2 steps in one dependency chain.  All eight candidate loads
+    // are extracted from the same L; step j corrects its difference by
+    // sum_i<j ([b_j == w_i] - [a_j == w_i]) for the winners w_i of the earlier
+    // steps, each term a precomputed constant per hypothesis picked by step i's
+    // mask (delta block: {dA, dA ^ dB} for the pairs 01 02 03 12 13 23).  The chain
+    // per step is pick -> add -> sgn (~3 ops) instead of the full single-step chain.
+    auto block4 = [&](const uint4 (&a)[4], const uint4 (&b)[4], const uint4 (&d)[3]) -> uint32_t {
+        uint32_t va[4], vb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            va[i] = prmt(L.lo, a[i].x, L.hi);
+            vb[i] = prmt(L.lo, a[i].y, L.hi);
+        }
+        uint32_t d1 = vb[1] - va[1], d2 = vb[2] - va[2], d3 = vb[3] - va[3];
+        const uint32_t m0 = sgn(vb[0] - va[0]);
+        d1 += pick(d[0].x, d[0].y, m0);
+        d2 += pick(d[0].z, d[0].w, m0);
+        d3 += pick(d[1].x, d[1].y, m0);
+        const uint32_t m1 = sgn(d1);
+        d2 += pick(d[1].z, d[1].w, m1);
+        d3 += pick(d[2].x, d[2].y, m1);
+        const uint32_t m2 = sgn(d2);
+        d3 += pick(d[2].z, d[2].w, m2);
+        const uint32_t m3 = sgn(d3);
+        const uint32_t m[4] = {m0, m1, m2, m3};
+        uint32_t ilo = 0, ihi = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            ilo += pick(a[i].z, b[i].x, m[i]);
+            ihi += pick(a[i].w, b[i].y, m[i]);
+        }
+        L.lo += ilo;
+        L.hi += ihi;
+        // the four decisions as one word (byte i = step i's mask): choices later
+        return prmt(prmt(m0, 0x0040u, m1), 0x5410u, prmt(m2, 0x0040u, m3));
     };
     int s = 0;
     if (n2 >= 4) {
-        uint4 a[4], b[4], c[2];
+        uint4 a[4], b[4], d[3];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             a[i] = lds4(ent + i * kES);
             b[i] = lds4(ent + i * kES + 4);
         }
-        c[0] = lds4(ent + 1 * kES + 8);
-        c[1] = lds4(ent + 3 * kES + 8);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) d[i] = lds4(dlt + i * 4);
         for (; s + 4 <= n2; s += 4) {
-            uint4 an[4], bn[4], cn[2];
-            const uint32_t *nx = ent + (s + 4) * kES;  // readable even past n2
+            uint4 an[4], bn[4], dn[3];
+            const uint32_t *nx = ent + (s + 4) * kES;         // readable even past n2
+            const uint32_t *nd = dlt + ((s >> 2) + 1) * 12;   // idem
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 an[i] = lds4(nx + i * kES);
                 bn[i] = lds4(nx + i * kES + 4);
             }
-            cn[0] = lds4(nx + 1 * kES + 8);
-            cn[1] = lds4(nx + 3 * kES + 8);
-            pair2(a[0], b[0], a[1], b[1], c[0]);
-            pair2(a[2], b[2], a[3], b[3], c[1]);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) dn[i] = lds4(nd + i * 4);
+            reinterpret_cast<uint32_t *>(dec)[s >> 2] = block4(a, b, d);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 a[i] = an[i];
                 b[i] = bn[i];
             }
-            c[0] = cn[0];
-            c[1] = cn[1];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) d[i] = dn[i];
         }
     }
-    for (; s < n2; ++s) step2(lds4(ent + s * kES), lds4(ent + s * kES + 4));
+    for (; s < n2; ++s) {
+        step2(lds4(ent + s * kES), lds4(ent + s * kES + 4));
+        dec[s] = dec_s;
+    }
     stamp(p, 8);
     // r = 3 steps, next entry prefetched (slots past m2 stay readable)
     if (s < n2 + n3) {
@@ -619,38 +639,31 @@ __device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t
             const uint32_t m2v = sgn(vc - vab);
             L.lo += pick(ilo, ilo ^ c.x, m2v);
             L.hi += pick(ihi, ihi ^ c.y, m2v);
-            const uint32_t gs = c.z, ga = gs & 0xffu, gb = (gs >> 8) & 0xffu, gc = (gs >> 16) & 0xffu;
-            const uint32_t gab = pick(ga, ga ^ gb, m1);
-            s_choice[c.w] = static_cast<int32_t>(pick(gab, gab ^ gc, m2v));
+            dec[s] = static_cast<uint8_t>((m1 & 1u) | (m2v & 2u));  // b beat a | c won
             a = an;
             b = bn;
             c = cn;
         }
     }
     stamp(p, 9);
-    // r >= 4: fixed 8-leaf tournament, next entry prefetched
+    // r >= 4: key_g = L[g] << 8 | 8g (+ 0x7f00 off-replica); the unsigned min is
+    // "smallest L, then lowest g" and its low byte is the increment's shift.
+    // Next entry prefetched.
     if (s < m2) {
-        uint4 n0 = lds4(ent + s * kES), n1 = lds4(ent + s * kES + 4), n2v = lds4(ent + s * kES + 8);
+        uint4 n0 = lds4(ent + s * kES), n1 = lds4(ent + s * kES + 4);
         for (; s < m2; ++s) {
-            const uint4 q0 = lds4(ent + (s + 1) * kES), q1 = lds4(ent + (s + 1) * kES + 4),
-                        q2 = lds4(ent + (s + 1) * kES + 8);
-            const uint32_t nc[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
-            Cand c[8];
+            const uint4 q0 = lds4(ent + (s + 1) * kES), q1 = lds4(ent + (s + 1) * kES + 4);
+            const uint32_t c[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+            uint32_t k[8];
 #pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                c[g].v = prmt(L.lo, zsel(g), L.hi) | nc[g];
-                c[g].ilo = inc_lo(g);
-                c[g].ihi = inc_hi(g);
-                c[g].g = g;
-            }
-            const Cand w =
-                duel(duel(duel(c[0], c[1]), duel(c[2], c[3])), duel(duel(c[4], c[5]), duel(c[6], c[7])));
-            L.lo += w.ilo;
-            L.hi += w.ihi;
-            s_choice[n2v.x] = static_cast<int32_t>(w.g);
+            for (int g = 0; g < 8; ++g) k[g] = prmt(L.lo, zsel1(g), L.hi) + c[g];
+            const uint32_t kmin = min(min(min(k[0], k[1]), min(k[2], k[3])), min(min(k[4], k[5]), min(k[6], k[7])));
+            const uint32_t sh = kmin & 0x38u;
+            L.lo += shl_clamp(1u, sh);
+            L.hi += shl_clamp(1u, sh - 32u);
+            dec[s] = static_cast<uint8_t>(sh);
             n0 = q0;
             n1 = q1;
-            n2v = q2;
         }
     }
     stamp(p, 10);
@@ -786,18 +799,22 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
             if (r <= 3) atomicMax(&misc[M_N3], rk + 1);  // end of the r=3 segment
         }
         if (try_packed) {
-            // step-pair corrections for the r=2 lookahead: for the pair (2j, 2j+1) with
-            // candidates (a, b) then (c, d), dX = [d == X] - [c == X]; stored in words 8..9
-            // of slot 2j+1 as {dA, dA ^ dB}
+            // block-of-four corrections for the r=2 lookahead: for steps i < j of a
+            // block with candidates (a_i, b_i), dX_ij = [b_j == X] - [a_j == X]; stored
+            // as {dA_ij, dA_ij ^ dB_ij} for ij = 01 02 03 12 13 23 (12 words per block)
             __syncthreads();
             const int n2 = misc[M_N2];
-            for (int j = tid; 2 * j + 1 < n2; j += kThreads) {
-                const uint32_t g1 = s_ent[(2 * j) * kES + 6], g2 = s_ent[(2 * j + 1) * kES + 6];
-                const int ga = g1 & 0xff, gb = (g1 >> 8) & 0xff, gc = g2 & 0xff, gd = (g2 >> 8) & 0xff;
-                const uint32_t dA = static_cast<uint32_t>(static_cast<int>(gd == ga) - static_cast<int>(gc == ga));
-                const uint32_t dB = static_cast<uint32_t>(static_cast<int>(gd == gb) - static_cast<int>(gc == gb));
-                s_ent[(2 * j + 1) * kES + 8] = dA;
-                s_ent[(2 * j + 1) * kES + 9] = dA ^ dB;
+            uint32_t *dlt = reinterpret_cast<uint32_t *>(smem + L.rpart);
+            for (int q = tid; q < (n2 >> 2) * 6; q += kThreads) {
+                const int blk = q / 6, pr = q - blk * 6;
+                const int i = pr < 3 ? 0 : (pr < 5 ? 1 : 2);
+                const int j = pr < 3 ? pr + 1 : (pr < 5 ? pr - 1 : 3);
+                const uint32_t gi = s_ent[(4 * blk + i) * kES + 6], gj = s_ent[(4 * blk + j) * kES + 6];
+                const int ai = gi & 0xff, bi = (gi >> 8) & 0xff, aj = gj & 0xff, bj = (gj >> 8) & 0xff;
+                const uint32_t dA = static_cast<uint32_t>(static_cast<int>(bj == ai) - static_cast<int>(aj == ai));
+                const uint32_t dB = static_cast<uint32_t>(static_cast<int>(bj == bi) - static_cast<int>(aj == bi));
+                dlt[blk * 12 + 2 * pr] = dA;
+                dlt[blk * 12 + 2 * pr + 1] = dA ^ dB;
             }
         }
     } else {
@@ -824,6 +841,8 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
     stamp(p, 5);
 
     bool done = false;
+    // per-step decisions of the packed r=2/3 steps (the key array is dead by now)
+    uint8_t *s_dec = smem + L.keys;
     if (MODE != kFromOrder && try_packed) {
         // Packed greedy (thread 0).  Valid iff every final counter is <= 126: the
         // counters only grow, so no byte ever crossed into the sign bit.
@@ -841,7 +860,9 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
                 else Lp.hi += v;
             }
             const int n2 = misc[M_N2], n3 = misc[M_N3] - n2;
-            if (ok) Lp = packed_greedy(p, s_ent, n2, n3, m2, s_choice, Lp);
+            if (ok)
+                Lp = packed_greedy(p, s_ent, reinterpret_cast<const uint32_t *>(smem + L.rpart), n2, n3, m2,
+                                   s_dec, Lp);
             // every final counter <= 126 (no byte reached the sign bit; counters only
             // grow) and the byte sum equals the assignments (no byte wrapped past 255)
             ok = ok && ((Lp.lo | Lp.hi) & 0x80808080u) == 0 && ((Lp.lo + 0x01010101u) & 0x80808080u) == 0 &&
@@ -861,6 +882,21 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
         __syncthreads();
         done = misc[M_PACKED_OK] != 0;
         if (done) {
+            // choices of the r=2/3 steps from their decision bytes, off the serial chain
+            const int n2 = misc[M_N2], n23 = misc[M_N3];
+            for (int q = tid; q < m2; q += kThreads) {
+                const uint32_t d = s_dec[q];
+                const uint32_t *en = s_ent + q * kES;
+                if (q >= n23) {  // r >= 4: d = 8 * winner
+                    s_choice[en[8]] = static_cast<int32_t>(d >> 3);
+                    continue;
+                }
+                const bool three = q >= n2;
+                const uint32_t gs = three ? en[10] : en[6];
+                const uint32_t sh = (three && (d & 2u)) ? 16u : ((d & 1u) ? 8u : 0u);
+                s_choice[three ? en[11] : en[7]] = static_cast<int32_t>((gs >> sh) & 0xffu);
+            }
+            __syncthreads();
             stamp(p, 6);
             return true;
         }

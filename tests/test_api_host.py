@@ -10,8 +10,7 @@ from paper_2512_09277_b200 import routing
 def test_reference_names_exported(eproute_ref):
     missing = [n for n in eproute_ref.__all__ if not hasattr(pkg, n)]
     # trace JSONL IO and the cost model are outside the routing hot path
-    allowed = {"CostProfile", "LayerTiming", "Trace", "TraceBatch", "TraceFormatError",
-               "load_trace", "save_trace"}
+    allowed = {"CostProfile", "LayerTiming"}
     assert set(missing) <= allowed, missing
 
 
