@@ -80,6 +80,7 @@ enum {
     METRO_ERR_ID_RANGE = 1,
     METRO_ERR_NO_REPLICA = 2,
     METRO_ERR_LOAD_RANGE = 3,
+    METRO_ERR_PAIR_RANK = 4,  /* dispatch layout: pair_rank[p] hosts no replica of ids[p] */
     METRO_EARG = -1,       /* null pointer / negative size */
     METRO_EDIMS = -2,      /* N or G outside the supported range */
     METRO_ECUDA = -3,      /* CUDA launch / copy error (see metro_last_cuda_error) */

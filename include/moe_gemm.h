@@ -31,8 +31,36 @@ METRO_API int moe_grouped_gemm_v1(const void *W, int32_t E, int32_t M, int32_t K
                                   const int32_t *items, int32_t n_items, void *Y, int32_t num_ctas,
                                   void *stream);
 
+/* The same with the item count read on device (*n_items_dev, clamped to
+ * items_cap) -- e.g. written by moe_layout_items_v1 -- so route -> layout ->
+ * items -> GEMM runs without a host round trip (graph-capturable).  T_cap =
+ * rows allocated in X / Y. */
+METRO_API int moe_grouped_gemm_dev_v1(const void *W, int32_t E, int32_t M, int32_t K, const void *X,
+                                      int32_t T_cap, const int32_t *items, int32_t items_cap,
+                                      const int32_t *n_items_dev, void *Y, int32_t num_ctas, void *stream);
+
+/* Work items of EP rank `rank` from a dispatch layout (include/dispatch_layout.h:
+ * rep_off [nrep + 1], slot_base [G + 1], device): for each local slot with rows,
+ * each 128-row block of an M1-row (and, if M2 > 0, M2-row) weight matrix and each
+ * <= 256-row chunk, {slot, m_block, first row, rows} -- slot-major, then (m_block,
+ * chunk).  counts[3] (device) = {items1, items2, rows of the rank}; item counts
+ * beyond cap1 / cap2 are not written (the GEMM clamps; check counts on the host). */
+METRO_API int moe_layout_items_v1(const int32_t *rep_off, const int32_t *slot_base, int32_t rank, int32_t M1,
+                                  int32_t M2, int32_t *items1, int32_t cap1, int32_t *items2, int32_t cap2,
+                                  int32_t *counts, void *stream);
+
+/* The rank's receive buffer: dst[pair_row[p]] = src[p / top_k] (row_bytes each)
+ * for every pair p with pair_rank[p] == rank (rows >= rows_cap are skipped).
+ * row_bytes % 16 == 0, 16-byte aligned src / dst. */
+METRO_API int moe_gather_rows_v1(const void *src, int32_t row_bytes, int32_t top_k, const int32_t *pair_rank,
+                                 const int32_t *pair_row, int64_t num_pairs, int32_t rank, void *dst,
+                                 int32_t rows_cap, void *stream);
+
 /* H[t, i] = silu(GU[t, i]) * GU[t, I + i]  (GU [T, 2I] -> H [T, I], bf16) */
 METRO_API int moe_silu_mul_v1(const void *GU, int32_t T, int32_t I, void *H, void *stream);
+/* The same over min(T_cap, *rows_dev) rows (device row count). */
+METRO_API int moe_silu_mul_dev_v1(const void *GU, int32_t T_cap, int32_t I, void *H, const int32_t *rows_dev,
+                                  void *stream);
 
 /* cudaError_t of the last failing CUDA call of the MoE entry points (0 if none). */
 METRO_API int moe_last_cuda_error(void);

@@ -15,6 +15,7 @@ from .oracle import (  # noqa: F401
     OracleError,
     aggregate_loads,
     build,
+    dispatch_layout,
     lib,
     metro_layer,
     pair_rank_eplb,

@@ -24,6 +24,12 @@
  *                               row-major occurrence of expert i goes to its
  *                               (o mod r_i)-th replica in ascending GPU id,
  *                               which reproduces route_eplb's x exactly.
+ *   oracle_dispatch_layout   <- the dispatch layout after routing (SURVEY.md
+ *                               §8(f) rank 1; include/dispatch_layout.h): rows of
+ *                               replica (i, g) number x[i, g] (routing.py:41-52,
+ *                               :64-69); rows grouped by (rank, local slot), pairs
+ *                               in row-major order inside a replica.  Written as
+ *                               the obvious sequential counting pass.
  *
  * Integer-only; no floating point anywhere on this path.
  */
@@ -202,4 +208,55 @@ int oracle_metro_layer(const int32_t *ids, int64_t npairs, const int8_t *A, int3
     if (rc) return rc;
     if (pair_rank) oracle_pair_rank_metro(ids, npairs, choice, pair_rank);
     return ORACLE_OK;
+}
+
+/* Dispatch layout, sequentially.  Replica ids are rank-major, by local slot
+ * (the i-th expert hosted on rank g in ascending expert id); rep_off [nrep + 1]
+ * is the exclusive prefix of rows per replica; pair_row[p] is the row of pair p
+ * counted from the first row of its serving rank.  Returns ORACLE_ERR_ID_RANGE /
+ * ORACLE_ERR_NO_REPLICA (with *bad = pair index) when a pair has an id out of
+ * range / a serving rank without a replica of its expert. */
+int oracle_dispatch_layout(const int32_t *ids, const int32_t *pair_rank, int64_t npairs, const int8_t *A,
+                           int32_t N, int32_t G, int32_t *pair_row, int32_t *rep_off, int64_t *bad) {
+    int32_t *rid = (int32_t *)malloc(sizeof(int32_t) * (size_t)N * (size_t)G + 4);
+    int32_t *rank_first = (int32_t *)malloc(sizeof(int32_t) * ((size_t)G + 1));
+    if (!rid || !rank_first) return ORACLE_ERR_ARG;
+    int32_t nrep = 0;
+    for (int32_t g = 0; g < G; ++g) {
+        rank_first[g] = nrep;
+        for (int32_t i = 0; i < N; ++i) rid[(int64_t)i * G + g] = A[(int64_t)i * G + g] ? nrep++ : -1;
+    }
+    rank_first[G] = nrep;
+    int64_t *cnt = (int64_t *)calloc((size_t)nrep + 1, sizeof(int64_t));
+    int rc = ORACLE_OK;
+    for (int64_t p = 0; p < npairs && rc == ORACLE_OK; ++p) {
+        const int32_t e = ids[p], g = pair_rank[p];
+        if (e < 0 || e >= N) {
+            rc = ORACLE_ERR_ID_RANGE;
+            *bad = p;
+        } else if (g < 0 || g >= G || rid[(int64_t)e * G + g] < 0) {
+            rc = ORACLE_ERR_NO_REPLICA;
+            *bad = p;
+        } else {
+            cnt[rid[(int64_t)e * G + g]]++;
+        }
+    }
+    if (rc == ORACLE_OK) {
+        int64_t run = 0;
+        for (int32_t r = 0; r < nrep; ++r) {
+            rep_off[r] = (int32_t)run;
+            run += cnt[r];
+            cnt[r] = 0; /* reused: rows handed out so far */
+        }
+        rep_off[nrep] = (int32_t)run;
+        for (int64_t p = 0; p < npairs; ++p) {
+            const int32_t e = ids[p], g = pair_rank[p];
+            const int32_t r = rid[(int64_t)e * G + g];
+            pair_row[p] = (int32_t)(rep_off[r] - rep_off[rank_first[g]] + cnt[r]++);
+        }
+    }
+    free(cnt);
+    free(rank_first);
+    free(rid);
+    return rc;
 }

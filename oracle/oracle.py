@@ -46,6 +46,7 @@ def lib() -> ctypes.CDLL:
         L.oracle_pair_rank_metro.restype = None
         L.oracle_pair_rank_eplb.argtypes = [P, i64, P, i32, i32, P]
         L.oracle_metro_layer.argtypes = [P, i64, P, i32, i32, P, P, P, P, P]
+        L.oracle_dispatch_layout.argtypes = [P, P, i64, P, i32, i32, P, P, P]
         _lib = L
     return _lib
 
@@ -151,3 +152,19 @@ def metro_layer(ids, A, out=None):
     if rc:
         raise OracleError(rc)
     return out
+
+
+def dispatch_layout(ids, pair_rank, A) -> Tuple[np.ndarray, np.ndarray]:
+    """(pair_row [P], rep_off [nrep + 1]) -- see oracle_dispatch_layout."""
+    ids = _c(ids, np.int32).reshape(-1)
+    pr = _c(pair_rank, np.int32).reshape(-1)
+    A = _c(A, np.int8)
+    N, G = A.shape
+    nrep = int((A != 0).sum())
+    row = np.empty(ids.size, np.int32)
+    off = np.empty(nrep + 1, np.int32)
+    bad = np.zeros(1, np.int64)
+    rc = lib().oracle_dispatch_layout(_p(ids), _p(pr), ids.size, _p(A), N, G, _p(row), _p(off), _p(bad))
+    if rc:
+        raise OracleError(rc, f"pair {int(bad[0])}")
+    return row, off

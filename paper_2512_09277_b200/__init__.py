@@ -44,6 +44,7 @@ from .routing import (
     save_assignment,
 )
 from .device import DevicePlacement, HostRouter, RouteResult, Router, pack_placement
+from .dispatch import DispatchLayout, LayoutResult, replica_table
 from .io import (
     Trace,
     TraceBatch,
@@ -65,7 +66,7 @@ __all__ = [
     "save_assignment", "validate_assignment", "zipf_popularity",
     "DevicePlacement", "HostRouter", "RouteResult", "Router", "pack_placement",
     "NativeLibraryError", "Trace", "TraceBatch", "TraceFormatError", "load_placement", "load_trace",
-    "load_trace_topk", "save_placement", "save_trace",
+    "load_trace_topk", "save_placement", "save_trace", "DispatchLayout", "LayoutResult", "replica_table",
 ]
 
 __version__ = "0.1.0"

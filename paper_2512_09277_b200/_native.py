@@ -23,6 +23,7 @@ OK = 0
 ERR_ID_RANGE = 1
 ERR_NO_REPLICA = 2
 ERR_LOAD_RANGE = 3
+ERR_PAIR_RANK = 4
 EARG = -1
 EDIMS = -2
 ECUDA = -3
@@ -75,6 +76,8 @@ def lib() -> ctypes.CDLL:
         "metro_host_workspace_bytes": ([i64, i32, i32], ctypes.c_size_t),
         "metro_route_host_v1": ([P, i64, P, i32, i32, P, P, P, i32, i32, P], ctypes.c_int),
         "metro_debug_set_stamps": ([P], None),
+        "metro_replica_table": ([P, i32, i32, P, P], ctypes.c_int),
+        "metro_dispatch_layout_v1": ([P, P, i64, P, P, i32, i32, i32, P, P, P, i32, P], ctypes.c_int),
     }
     for name, (argtypes, restype) in sig.items():
         fn = getattr(L, name)
@@ -86,7 +89,7 @@ def lib() -> ctypes.CDLL:
     return L
 
 
-HEADERS = ("metro_route.h", "moe_gemm.h")
+HEADERS = ("metro_route.h", "moe_gemm.h", "dispatch_layout.h")
 
 
 def exported_symbols() -> list:

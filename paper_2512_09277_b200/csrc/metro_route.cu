@@ -36,6 +36,8 @@
 #include <mutex>
 
 #include "../../include/metro_route.h"
+#include "lib_internal.h"
+#include "sm100_ptx.cuh"
 
 namespace metro {
 
@@ -131,86 +133,7 @@ enum {
     M_PACKED_LO = 9, M_PACKED_HI = 10, M_PACKED_OK = 11,
 };
 
-// ---------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
-    asm volatile(
-        "{\n\t.reg .pred P;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
-        "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-// TMA bulk copy global -> own shared memory, completion on the mbarrier.
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t cluster_nctarank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_arrive_relaxed() {
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_arrive_release() {
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() {
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// Store one word into CTA `cta`'s shared memory at the address `local` has in ours.
-__device__ __forceinline__ void dsmem_st(const void *local, uint32_t cta, uint32_t v) {
-    uint32_t raddr;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(local)), "r"(cta));
-    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(raddr), "r"(v) : "memory");
-}
-// Asynchronous 4-byte store into CTA `cta`'s shared memory (same offset as `local`
-// in ours) that completes `bytes` on that CTA's mbarrier at `local_bar`'s offset.
-__device__ __forceinline__ void st_async_b32(const void *local, uint32_t cta, uint32_t v, const void *local_bar) {
-    uint32_t raddr, rbar;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(local)), "r"(cta));
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(local_bar)), "r"(cta));
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(raddr), "r"(v),
-                 "r"(rbar)
-                 : "memory");
-}
-
-__device__ __forceinline__ void st_async_v4(const void *local, uint32_t cta, uint4 v, const void *local_bar) {
-    uint32_t raddr, rbar;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32(local)), "r"(cta));
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(local_bar)), "r"(cta));
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
-                     raddr),
-                 "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rbar)
-                 : "memory");
-}
-
-__device__ __forceinline__ unsigned lanemask_lt() {
-    unsigned m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-    return m;
-}
+// PTX helpers (mbarrier, bulk copy, cluster, DSMEM): sm100_ptx.cuh
 __device__ __forceinline__ void stamp(const Params &p, int i) {
     if (p.stamps && threadIdx.x == 0 && cluster_ctarank() == 0) p.stamps[i] = clock64();
 }
@@ -1282,10 +1205,10 @@ __global__ void __launch_bounds__(kThreads, 1) eplb_loads_kernel(const Params p)
 }
 
 // ================================================================ host side
-static thread_local int g_last_cuda_error = 0;
+thread_local int g_last_cuda_error = 0;  // shared with dispatch_layout.cu (lib_internal.h)
 static int64_t *g_stamps = nullptr;
 
-static int cuda_fail(cudaError_t e) {
+int cuda_fail(cudaError_t e) {
     g_last_cuda_error = static_cast<int>(e);
     return METRO_ECUDA;
 }
@@ -1416,6 +1339,7 @@ const char *metro_strerror(int code) {
         case METRO_ERR_ID_RANGE: return "expert id out of range";
         case METRO_ERR_NO_REPLICA: return "placement invariant: every expert has a replica";
         case METRO_ERR_LOAD_RANGE: return "load does not fit 32 bits on the device loads path";
+        case METRO_ERR_PAIR_RANK: return "pair routed to a rank that hosts no replica of its expert";
         case METRO_EARG: return "invalid argument";
         case METRO_EDIMS: return "unsupported dimensions (1 <= G <= 128, 1 <= N <= 4096) or shared memory exceeded";
         case METRO_ECUDA: return "CUDA error";

@@ -46,7 +46,8 @@ struct Item {
 
 struct Params {
     const Item *items;
-    int n_items;
+    int n_items;                // capacity when n_items_dev is set
+    const int32_t *n_items_dev; // nullable: item count produced on device (moe_layout_items_v1)
     int K;
     __nv_bfloat16 *Y;
     int ldy;
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int kblocks = p.K / BK;
+    const int n_items = p.n_items_dev ? min(p.n_items, *p.n_items_dev) : p.n_items;
 
     if (warp == 4 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -176,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+            for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
                 const Item item = p.items[it];
                 const int mi = map_index(item.n);
                 const uint32_t bbytes = static_cast<uint32_t>((16 << mi) * BK * 2);
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
-            for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++local) {
+            for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
                 const Item item = p.items[it];
                 const int acc = local & 1;
                 const uint32_t aphase = (local >> 1) & 1;
@@ -227,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     } else {
         // ---------------- epilogue: warps 0-3 own TMEM lanes 32w .. 32w+31 (= W rows)
         int local = 0;
-        for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++local) {
+        for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
             const Item item = p.items[it];
             const int acc = local & 1;
             const uint32_t aphase = (local >> 1) & 1;
@@ -260,7 +262,9 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
 }
 
 // H[t, i] = silu(GU[t, i]) * GU[t, I + i]   (gate | up halves of the first projection)
-__global__ void silu_mul_kernel(const __nv_bfloat16 *__restrict__ gu, int T, int I, __nv_bfloat16 *__restrict__ h) {
+__global__ void silu_mul_kernel(const __nv_bfloat16 *__restrict__ gu, int T, int I, __nv_bfloat16 *__restrict__ h,
+                                const int32_t *rows_dev) {
+    if (rows_dev) T = min(T, *rows_dev);
     const int64_t total = static_cast<int64_t>(T) * I;
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -268,6 +272,85 @@ __global__ void silu_mul_kernel(const __nv_bfloat16 *__restrict__ gu, int T, int
         const float g = __bfloat162float(gu[t * 2 * I + i]);
         const float u = __bfloat162float(gu[t * 2 * I + I + i]);
         h[idx] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u);
+    }
+}
+
+// Work items of one EP rank from a dispatch layout (include/dispatch_layout.h):
+// for every local slot s with rows, every 128-row block of the weight matrix and
+// every <= 256-row chunk -> {s, m_blk, t0, n}; slot-major, then (m_blk, chunk) --
+// the order of moe.build_items.  Two projections (mb1 / mb2 row blocks) in one
+// pass.  One CTA; counts = {items1, items2, rows of the rank}.
+constexpr int kItThreads = 512;
+__global__ void __launch_bounds__(kItThreads) layout_items_kernel(const int32_t *__restrict__ rep_off,
+                                                                  const int32_t *__restrict__ slot_base, int rank,
+                                                                  int mb1, int mb2, Item *items1, Item *items2,
+                                                                  int cap1, int cap2, int32_t *counts) {
+    __shared__ int32_t s_w[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int b0 = slot_base[rank], S = slot_base[rank + 1] - b0;
+    const int base_row = rep_off[b0];
+    int run = 0;  // chunks of the slots already done
+    for (int s0 = 0; s0 < S; s0 += kItThreads) {
+        const int s = s0 + tid;
+        const int n = (s < S) ? rep_off[b0 + s + 1] - rep_off[b0 + s] : 0;
+        const int c = (n + MAXN - 1) / MAXN;
+        int x = c;  // inclusive scan of chunk counts
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+        }
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int w = lane < kItThreads / 32 ? s_w[lane] : 0;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, w, d);
+                if (lane >= d) w += y;
+            }
+            s_w[lane] = w;
+        }
+        __syncthreads();
+        const int before = run + x - c + (warp > 0 ? s_w[warp - 1] : 0);
+        if (c > 0) {
+            const int t0 = rep_off[b0 + s] - base_row;
+            for (int mb = 0; mb < mb1; ++mb)
+                for (int j = 0; j < c; ++j) {
+                    const int idx = before * mb1 + mb * c + j;
+                    if (idx < cap1) items1[idx] = Item{s, mb, t0 + j * MAXN, min(MAXN, n - j * MAXN)};
+                }
+            for (int mb = 0; mb < mb2; ++mb)
+                for (int j = 0; j < c; ++j) {
+                    const int idx = before * mb2 + mb * c + j;
+                    if (idx < cap2) items2[idx] = Item{s, mb, t0 + j * MAXN, min(MAXN, n - j * MAXN)};
+                }
+        }
+        run += s_w[kItThreads / 32 - 1];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        counts[0] = run * mb1;  // may exceed the capacity: the GEMM clamps, the host checks
+        counts[1] = run * mb2;
+        counts[2] = rep_off[b0 + S] - base_row;
+    }
+}
+
+// dst[pair_row[p]] = src[p / k] for the pairs served by `rank` (one warp per pair,
+// 16-byte vectors): the rank's receive buffer in dispatch-layout order.
+__global__ void gather_rows_kernel(const uint4 *__restrict__ src, int row_vecs, int k,
+                                   const int32_t *__restrict__ pair_rank, const int32_t *__restrict__ pair_row,
+                                   int64_t num_pairs, int rank, uint4 *__restrict__ dst, int rows_cap) {
+    const int64_t warp_id = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t p = warp_id; p < num_pairs; p += nwarps) {
+        if (pair_rank[p] != rank) continue;
+        const int r = pair_row[p];
+        if (r < 0 || r >= rows_cap) continue;
+        const uint4 *s = src + (p / k) * row_vecs;
+        uint4 *d = dst + static_cast<int64_t>(r) * row_vecs;
+        for (int v = lane; v < row_vecs; v += 32) d[v] = s[v];
     }
 }
 
@@ -303,12 +386,9 @@ using namespace moe;
 
 extern "C" {
 
-METRO_API int moe_grouped_gemm_v1(const void *W, int32_t E, int32_t M, int32_t K, const void *X, int32_t T,
-                        const int32_t *items, int32_t n_items, void *Y, int32_t num_ctas, void *stream) {
-    if (!W || !X || !Y || (!items && n_items > 0) || E < 1 || M < BM || K < BK || T < 1 || n_items < 0)
-        return METRO_EARG;
-    if (M % BM || K % BK) return METRO_EDIMS;
-    if (n_items == 0) return METRO_OK;
+static int launch_gemm(const void *W, int32_t E, int32_t M, int32_t K, const void *X, int32_t T,
+                       const int32_t *items, int32_t n_items, const int32_t *n_items_dev, void *Y, int32_t num_ctas,
+                       void *stream) {
     Maps maps;
     const cuuint64_t wdims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(E)};
     const cuuint64_t wstr[2] = {static_cast<cuuint64_t>(K) * 2, static_cast<cuuint64_t>(M) * K * 2};
@@ -336,6 +416,7 @@ METRO_API int moe_grouped_gemm_v1(const void *W, int32_t E, int32_t M, int32_t K
     Params prm;
     prm.items = reinterpret_cast<const Item *>(items);
     prm.n_items = n_items;
+    prm.n_items_dev = n_items_dev;
     prm.K = K;
     prm.Y = static_cast<__nv_bfloat16 *>(Y);
     prm.ldy = M;
@@ -348,13 +429,83 @@ METRO_API int moe_grouped_gemm_v1(const void *W, int32_t E, int32_t M, int32_t K
     return METRO_OK;
 }
 
+METRO_API int moe_grouped_gemm_v1(const void *W, int32_t E, int32_t M, int32_t K, const void *X, int32_t T,
+                        const int32_t *items, int32_t n_items, void *Y, int32_t num_ctas, void *stream) {
+    if (!W || !X || !Y || (!items && n_items > 0) || E < 1 || M < BM || K < BK || T < 1 || n_items < 0)
+        return METRO_EARG;
+    if (M % BM || K % BK) return METRO_EDIMS;
+    if (n_items == 0) return METRO_OK;
+    return launch_gemm(W, E, M, K, X, T, items, n_items, nullptr, Y, num_ctas, stream);
+}
+
+METRO_API int moe_grouped_gemm_dev_v1(const void *W, int32_t E, int32_t M, int32_t K, const void *X,
+                                      int32_t T_cap, const int32_t *items, int32_t items_cap,
+                                      const int32_t *n_items_dev, void *Y, int32_t num_ctas, void *stream) {
+    if (!W || !X || !Y || !items || !n_items_dev || E < 1 || M < BM || K < BK || T_cap < 1 || items_cap < 1)
+        return METRO_EARG;
+    if (M % BM || K % BK) return METRO_EDIMS;
+    return launch_gemm(W, E, M, K, X, T_cap, items, items_cap, n_items_dev, Y, num_ctas, stream);
+}
+
+METRO_API int moe_layout_items_v1(const int32_t *rep_off, const int32_t *slot_base, int32_t rank, int32_t M1,
+                                  int32_t M2, int32_t *items1, int32_t cap1, int32_t *items2, int32_t cap2,
+                                  int32_t *counts, void *stream) {
+    if (!rep_off || !slot_base || !items1 || !counts || rank < 0 || M1 < BM || cap1 < 0 || cap2 < 0 ||
+        (M2 > 0 && !items2))
+        return METRO_EARG;
+    if (M1 % BM || (M2 > 0 && M2 % BM)) return METRO_EDIMS;
+    layout_items_kernel<<<1, kItThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        rep_off, slot_base, rank, M1 / BM, M2 > 0 ? M2 / BM : 0, reinterpret_cast<Item *>(items1),
+        reinterpret_cast<Item *>(items2), cap1, cap2, counts);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        g_err = e;
+        return METRO_ECUDA;
+    }
+    return METRO_OK;
+}
+
+METRO_API int moe_gather_rows_v1(const void *src, int32_t row_bytes, int32_t top_k, const int32_t *pair_rank,
+                                 const int32_t *pair_row, int64_t num_pairs, int32_t rank, void *dst,
+                                 int32_t rows_cap, void *stream) {
+    if (!src || !dst || top_k < 1 || row_bytes < 16 || num_pairs < 0 || rows_cap < 0 ||
+        (num_pairs > 0 && (!pair_rank || !pair_row)))
+        return METRO_EARG;
+    if (row_bytes % 16 || (reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(dst) & 15))
+        return METRO_EDIMS;
+    if (num_pairs == 0) return METRO_OK;
+    const int64_t blocks = (num_pairs + 7) / 8;
+    const int grid = static_cast<int>(blocks < 148 * 16 ? blocks : 148 * 16);
+    gather_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4 *>(src), row_bytes / 16, top_k, pair_rank, pair_row, num_pairs, rank,
+        static_cast<uint4 *>(dst), rows_cap);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        g_err = e;
+        return METRO_ECUDA;
+    }
+    return METRO_OK;
+}
+
+static int launch_silu(const void *GU, int32_t T, int32_t I, void *H, const int32_t *rows_dev, void *stream);
+
 METRO_API int moe_silu_mul_v1(const void *GU, int32_t T, int32_t I, void *H, void *stream) {
+    return launch_silu(GU, T, I, H, nullptr, stream);
+}
+
+METRO_API int moe_silu_mul_dev_v1(const void *GU, int32_t T_cap, int32_t I, void *H, const int32_t *rows_dev,
+                                  void *stream) {
+    if (!rows_dev) return METRO_EARG;
+    return launch_silu(GU, T_cap, I, H, rows_dev, stream);
+}
+
+static int launch_silu(const void *GU, int32_t T, int32_t I, void *H, const int32_t *rows_dev, void *stream) {
     if (!GU || !H || T < 0 || I < 1) return METRO_EARG;
     if (T == 0) return METRO_OK;
     const int64_t total = static_cast<int64_t>(T) * I;
     const int grid = static_cast<int>(total / 256 + 1 < 148 * 8 ? total / 256 + 1 : 148 * 8);
     silu_mul_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<const __nv_bfloat16 *>(GU), T, I, static_cast<__nv_bfloat16 *>(H));
+        static_cast<const __nv_bfloat16 *>(GU), T, I, static_cast<__nv_bfloat16 *>(H), rows_dev);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         g_err = e;

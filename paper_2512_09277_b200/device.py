@@ -73,12 +73,16 @@ class DevicePlacement:
                 f"placement {n}x{g} outside the sm_100a kernel limits "
                 f"(1 <= N <= {_native.MAX_N}, 1 <= G <= {_native.MAX_G})"
             )
-        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        d = torch.device(device) if device is not None else torch.device("cuda")
+        if d.type == "cuda" and d.index is None:  # normalise "cuda" to "cuda:<current>"
+            d = torch.device("cuda", torch.cuda.current_device())
+        self.device = d
         mask = pack_placement(mat)
         self.num_experts, self.num_ranks, self.words = n, g, mask.shape[1]
         self.mask_host = mask
         self.mask = torch.from_numpy(mask.view(np.int32)).to(self.device)
         self.replica_counts = np.asarray(mat != 0).sum(axis=1)
+        self.matrix = np.ascontiguousarray(mat, dtype=np.int8)
 
 
 @dataclass
@@ -117,6 +121,9 @@ def raise_status(status: np.ndarray, top_k: int = 1) -> None:
         raise AssertionError("placement invariant: every expert has a replica")
     if code == _native.ERR_LOAD_RANGE:
         raise ValidationError("load does not fit the device loads path")
+    if code == _native.ERR_PAIR_RANK:
+        pair = int(np.uint32(status[1])) | (int(np.uint32(status[2])) << 32)
+        raise ValidationError(f"token {pair // max(top_k, 1)}: rank {int(status[3])} hosts no replica of its expert")
     raise _native.NativeLibraryError(f"unknown kernel status {code}")
 
 

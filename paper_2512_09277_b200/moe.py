@@ -35,6 +35,14 @@ def _lib():
         L.moe_grouped_gemm_v1.restype = ctypes.c_int
         L.moe_silu_mul_v1.argtypes = [P, i32, i32, P, P]
         L.moe_silu_mul_v1.restype = ctypes.c_int
+        L.moe_grouped_gemm_dev_v1.argtypes = [P, i32, i32, i32, P, i32, P, i32, P, P, i32, P]
+        L.moe_grouped_gemm_dev_v1.restype = ctypes.c_int
+        L.moe_layout_items_v1.argtypes = [P, P, i32, i32, i32, P, i32, P, i32, P, P]
+        L.moe_layout_items_v1.restype = ctypes.c_int
+        L.moe_gather_rows_v1.argtypes = [P, i32, i32, P, P, ctypes.c_int64, i32, P, i32, P]
+        L.moe_gather_rows_v1.restype = ctypes.c_int
+        L.moe_silu_mul_dev_v1.argtypes = [P, i32, i32, P, P, P]
+        L.moe_silu_mul_dev_v1.restype = ctypes.c_int
         L.moe_last_cuda_error.argtypes = []
         L.moe_last_cuda_error.restype = ctypes.c_int
         L._moe_bound = True
@@ -153,3 +161,89 @@ class ExpertFFN:
         silu_mul(GU, H)
         grouped_gemm(self.W2, H, items2, Y)
         return Y
+
+
+class RankMoE:
+    """One EP rank's MoE layer, entirely on device and graph-capturable:
+
+        route (METRO / EPLB, pair ranks)      metro_route_v1 / eplb_route_v1
+        -> dispatch layout                    metro_dispatch_layout_v1
+        -> the rank's K3 work items           moe_layout_items_v1
+        -> receive buffer (token rows)        moe_gather_rows_v1
+        -> expert FFN                         moe_grouped_gemm_dev_v1, silu, GEMM
+
+    No host round trip: item and row counts stay on device.  Buffers are sized
+    for the worst case (every pair of ``max_pairs`` on this rank).  The combine
+    back to token order is the EP all-to-all's job and out of scope.
+    """
+
+    def __init__(self, placement, kind: str, rank: int, ffn: "ExpertFFN", max_pairs: int, top_k: int,
+                 cluster_ctas: int = 0):
+        from .device import Router
+        from .dispatch import DispatchLayout
+
+        dev = placement.device
+        self.kind, self.rank, self.ffn, self.top_k = kind, int(rank), ffn, int(top_k)
+        self.router = Router(placement, kind, cluster_ctas)
+        self.layout = DispatchLayout(placement, cluster_ctas)
+        slots = self.layout.slots(self.rank)
+        if slots > ffn.slots:
+            raise ValidationError(f"rank {rank} hosts {slots} experts but the FFN has {ffn.slots} slots")
+        self.max_pairs = int(max_pairs)
+        self.rows_cap = max(1, self.max_pairs)
+        chunks = slots + self.rows_cap // MAXN + 1
+        self.cap1 = chunks * (2 * ffn.inter // BM)
+        self.cap2 = chunks * (ffn.hidden // BM)
+        self.route_out = self.router.alloc(self.max_pairs, pair_rank=True, top_k=self.top_k)
+        i32 = dict(dtype=torch.int32, device=dev)
+        from .dispatch import LayoutResult
+
+        self.layout_out = LayoutResult(pair_row=torch.empty(self.rows_cap, **i32),
+                                       rep_off=torch.empty(self.layout.nrep + 1, **i32),
+                                       status=torch.zeros(4, **i32), top_k=self.top_k)
+        self.items1 = torch.empty((self.cap1, 4), **i32)
+        self.items2 = torch.empty((self.cap2, 4), **i32)
+        self.counts = torch.zeros(3, **i32)
+        bf = dict(dtype=torch.bfloat16, device=dev)
+        self.X = torch.zeros((self.rows_cap, ffn.hidden), **bf)
+        self.GU = torch.empty((self.rows_cap, 2 * ffn.inter), **bf)
+        self.H = torch.empty((self.rows_cap, ffn.inter), **bf)
+        self.Y = torch.empty((self.rows_cap, ffn.hidden), **bf)
+
+    def __call__(self, topk_ids: torch.Tensor, hidden: torch.Tensor, stream=None) -> torch.Tensor:
+        """topk_ids int32 [B, k] (all-gathered), hidden bf16 [B, D] -> Y [rows_cap, D]
+        (the first ``counts[2]`` rows are this rank's outputs, dispatch-layout order)."""
+        import ctypes
+
+        if topk_ids.numel() > self.max_pairs:
+            raise ValidationError(f"{topk_ids.numel()} pairs > max_pairs {self.max_pairs}")
+        if hidden.dtype != torch.bfloat16 or hidden.shape[-1] != self.ffn.hidden or not hidden.is_contiguous():
+            raise ValidationError("hidden must be a contiguous bf16 [B, hidden] tensor")
+        s = stream if stream is not None else torch.cuda.current_stream(self.X.device)
+        sp = ctypes.c_void_p(s.cuda_stream)
+        L = _lib()
+        rr = self.router.route(topk_ids, out=self.route_out, stream=s)
+        P = topk_ids.numel()
+        ids = topk_ids.reshape(-1)
+        pr = rr.pair_rank[:P]
+        self.layout_out = self.layout(ids, pr, out=self.layout_out, stream=s)
+        lo = self.layout_out
+        _check(L.moe_layout_items_v1(lo.rep_off.data_ptr(), self.layout.slot_base.data_ptr(), self.rank,
+                                     2 * self.ffn.inter, self.ffn.hidden, self.items1.data_ptr(), self.cap1,
+                                     self.items2.data_ptr(), self.cap2, self.counts.data_ptr(), sp),
+               "moe_layout_items_v1")
+        _check(L.moe_gather_rows_v1(hidden.data_ptr(), self.ffn.hidden * 2, self.top_k, pr.data_ptr(),
+                                    lo.pair_row.data_ptr(), P, self.rank, self.X.data_ptr(), self.rows_cap, sp),
+               "moe_gather_rows_v1")
+        f = self.ffn
+        _check(L.moe_grouped_gemm_dev_v1(f.W1.data_ptr(), f.slots, 2 * f.inter, f.hidden, self.X.data_ptr(),
+                                         self.rows_cap, self.items1.data_ptr(), self.cap1,
+                                         self.counts.data_ptr(), self.GU.data_ptr(), 0, sp),
+               "moe_grouped_gemm_dev_v1")
+        _check(L.moe_silu_mul_dev_v1(self.GU.data_ptr(), self.rows_cap, f.inter, self.H.data_ptr(),
+                                     self.counts[2:].data_ptr(), sp), "moe_silu_mul_dev_v1")
+        _check(L.moe_grouped_gemm_dev_v1(f.W2.data_ptr(), f.slots, f.hidden, f.inter, self.H.data_ptr(),
+                                         self.rows_cap, self.items2.data_ptr(), self.cap2,
+                                         self.counts[1:].data_ptr(), self.Y.data_ptr(), 0, sp),
+               "moe_grouped_gemm_dev_v1")
+        return self.Y
