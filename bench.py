@@ -484,6 +484,9 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
             "metro": m["metro"], "eplb": m["eplb"],
             "ffn_speedup_metro_vs_eplb": m["ffn_speedup_metro_vs_eplb"],
             "weight_byte_ratio_eplb_over_metro": m["weight_byte_ratio_eplb_over_metro"],
+            "device_layer_speedup_metro_vs_eplb": m["device_layer_speedup_metro_vs_eplb"],
+            "device_layer_what": "the same rank's whole layer in one CUDA graph: route -> dispatch layout -> "
+                                 "K3 work items -> row gather -> FFN, no host round trip",
             "roofline": {"bound": "hbm", "achieved": m["metro"]["achieved_gbs"], "peak": m["peak_gbs"],
                          "unit": "GB/s", "frac": m["metro"]["frac"], "kernel": "moe_gemm_kernel"},
         }

@@ -48,6 +48,29 @@ def time_ffn(ffn, X, i1, i2, bufs, reps):
     return statistics.median(ts)
 
 
+def time_graph(fn, reps, inner=1):
+    """Median per-call device time of ``fn`` captured ``inner`` times in one CUDA graph."""
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        fn(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(inner):
+                fn(s)
+    g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e3 / inner)
+    return statistics.median(ts)
+
+
 def run(batches=4, reps=5, B=1024, ratio=1.5, seed0=1000):
     dev = torch.device("cuda", 0)
     N, k, G = 256, 8, 8
@@ -81,13 +104,28 @@ def run(batches=4, reps=5, B=1024, ratio=1.5, seed0=1000):
             res[kind] = {"rank": g, "activated": wl.activated, "tokens": wl.tokens, "ffn_us": us,
                          "weight_bytes": wbytes, "achieved_gbs": (wbytes + abytes) / (us * 1e-6) / 1e9}
             res[kind]["frac"] = res[kind]["achieved_gbs"] / pk
+            # the same rank's whole layer on device, one CUDA graph: route -> dispatch
+            # layout -> work items -> row gather -> FFN (no host round trip)
+            pipe = moe.RankMoE(pl, kind, g, ffn, max_pairs=B * k, top_k=k)
+            hidden = torch.randn((B, HIDDEN), device=dev).to(torch.bfloat16)
+            res[kind]["device_layer_us"] = time_graph(lambda st: pipe(ids, hidden, stream=st), reps)
+            if int(pipe.counts[2].item()) != wl.tokens:
+                raise RuntimeError("device layout rows differ from the host workload")
+            lay = pipe.layout
+            pr = pipe.route_out.pair_rank[: ids.numel()]
+            lout = pipe.layout_out
+            res[kind]["dispatch_layout_us"] = time_graph(
+                lambda st: lay(ids, pr, out=lout, stream=st), reps, inner=200)
+            del pipe
         rows.append(res)
         print(json.dumps(res), flush=True)
     summ = {}
     for kind in ("metro", "eplb"):
         summ[kind] = {key: statistics.mean(r[kind][key] for r in rows)
-                      for key in ("activated", "tokens", "ffn_us", "weight_bytes", "achieved_gbs", "frac")}
+                      for key in ("activated", "tokens", "ffn_us", "weight_bytes", "achieved_gbs", "frac",
+                                  "device_layer_us", "dispatch_layout_us")}
     summ["ffn_speedup_metro_vs_eplb"] = summ["eplb"]["ffn_us"] / summ["metro"]["ffn_us"]
+    summ["device_layer_speedup_metro_vs_eplb"] = summ["eplb"]["device_layer_us"] / summ["metro"]["device_layer_us"]
     summ["weight_byte_ratio_eplb_over_metro"] = summ["eplb"]["weight_bytes"] / summ["metro"]["weight_bytes"]
     summ["peak_gbs"] = pk
     summ["peak_source"] = pk_src
