@@ -21,6 +21,9 @@
  *   eplb_route_v1             <- core.py:236-244 + routing.py:55-72 route_eplb
  *   eplb_route_from_loads_v1  <- routing.py:55-72 route_eplb(T, A)
  *   metro_aggregate_loads_v1  <- core.py:236-244 aggregate_loads alone
+ *   metro_route_scores_v1     <- the gating top-k (core.py:319-326, the
+ *                                reference's generator of top-k ids) fused with
+ *                                metro_route_v1
  *   metro_pack_placement      <- core.py:84-119 PlacementMap (binary A -> bitmasks)
  *   metro_route_host_v1       <- the same as metro_route_v1 from HOST buffers
  *                                (H2D, kernel, D2H, sync) -- the e2e call
@@ -105,6 +108,19 @@ METRO_API int metro_route_v1(const int32_t *topk_ids, int64_t num_pairs, const u
                    int32_t num_experts, int32_t num_ranks, int32_t *loads, int32_t *choice,
                    int32_t *rank_counts, int32_t *lam, int32_t *pair_rank, int32_t *status,
                    int32_t cluster_ctas, void *stream);
+
+/* Gating top-k fused with METRO.  scores [num_tokens, N]
+ * fp32 router scores of the all-gathered tokens; each token's top_k experts --
+ * largest score first, ties to the lower expert id, the descending-key order of
+ * the reference's generator (core.py:319-326) -- are written to topk_ids
+ * [num_tokens, top_k] and routed in the same launch (no separate pass over the
+ * ids).  Other outputs as metro_route_v1.  Limits: N <= 512, G <= 32,
+ * top_k <= 32, top_k <= N; NaN scores are not supported. */
+METRO_API int metro_route_scores_v1(const float *scores, int64_t num_tokens, int32_t top_k,
+                                    const uint32_t *rank_mask, int32_t num_experts, int32_t num_ranks,
+                                    int32_t *topk_ids, int32_t *loads, int32_t *choice, int32_t *rank_counts,
+                                    int32_t *lam, int32_t *pair_rank, int32_t *status, int32_t cluster_ctas,
+                                    void *stream);
 
 /* aggregate_loads only (core.py:236-244): loads[N] from the ids; status as above. */
 METRO_API int metro_aggregate_loads_v1(const int32_t *topk_ids, int64_t num_pairs,

@@ -16,6 +16,7 @@ from .oracle import (  # noqa: F401
     aggregate_loads,
     build,
     dispatch_layout,
+    gate_topk,
     lib,
     metro_layer,
     pair_rank_eplb,

@@ -24,6 +24,12 @@
  *                               row-major occurrence of expert i goes to its
  *                               (o mod r_i)-th replica in ascending GPU id,
  *                               which reproduces route_eplb's x exactly.
+ *   oracle_gate_topk         <- the top-k selection of the reference's batch
+ *                               generator (core.py:319-326: argpartition of the
+ *                               negated scores, then descending by score) -- the
+ *                               gating step fused into metro_route_scores_v1.
+ *                               Ties (measure zero for the reference's continuous
+ *                               scores) go to the lower expert id.
  *   oracle_dispatch_layout   <- the dispatch layout after routing (SURVEY.md
  *                               §8(f) rank 1; include/dispatch_layout.h): rows of
  *                               replica (i, g) number x[i, g] (routing.py:41-52,
@@ -259,4 +265,22 @@ int oracle_dispatch_layout(const int32_t *ids, const int32_t *pair_rank, int64_t
     free(rank_first);
     free(rid);
     return rc;
+}
+
+/* Top-k of each token's scores, largest first; equal scores -> lower expert id.
+ * Written as k rounds of "first maximum" over the not-yet-taken experts. */
+void oracle_gate_topk(const float *scores, int64_t T, int32_t N, int32_t k, int32_t *ids) {
+    unsigned char *taken = (unsigned char *)malloc((size_t)N + 1);
+    for (int64_t t = 0; t < T; ++t) {
+        const float *row = scores + t * N;
+        memset(taken, 0, (size_t)N);
+        for (int32_t r = 0; r < k; ++r) {
+            int32_t best = -1;
+            for (int32_t e = 0; e < N; ++e)
+                if (!taken[e] && (best < 0 || row[e] > row[best])) best = e;
+            taken[best] = 1;
+            ids[t * k + r] = best;
+        }
+    }
+    free(taken);
 }

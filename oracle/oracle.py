@@ -47,6 +47,8 @@ def lib() -> ctypes.CDLL:
         L.oracle_pair_rank_eplb.argtypes = [P, i64, P, i32, i32, P]
         L.oracle_metro_layer.argtypes = [P, i64, P, i32, i32, P, P, P, P, P]
         L.oracle_dispatch_layout.argtypes = [P, P, i64, P, i32, i32, P, P, P]
+        L.oracle_gate_topk.argtypes = [P, i64, i32, i32, P]
+        L.oracle_gate_topk.restype = None
         _lib = L
     return _lib
 
@@ -168,3 +170,14 @@ def dispatch_layout(ids, pair_rank, A) -> Tuple[np.ndarray, np.ndarray]:
     if rc:
         raise OracleError(rc, f"pair {int(bad[0])}")
     return row, off
+
+
+def gate_topk(scores, k: int) -> np.ndarray:
+    """int32 [T, k]: each row's k largest scores' expert ids, largest first."""
+    sc = _c(scores, np.float32)
+    T, N = sc.shape
+    if not 1 <= k <= N:
+        raise OracleError(3, "k out of range")
+    ids = np.empty((T, k), np.int32)
+    lib().oracle_gate_topk(_p(sc), T, N, k, _p(ids))
+    return ids

@@ -73,6 +73,12 @@ struct Params {
     int32_t *x32;
     int64_t *x64;
     int64_t *stamps;
+    // gating mode (metro_route_scores_v1): router scores [num_tokens, N] fp32 in,
+    // top-k ids [num_tokens, top_k] out; ids = nullptr
+    const float *scores;
+    int64_t num_tokens;
+    int32_t top_k;
+    int32_t *ids_out;
 };
 
 // ---------------------------------------------------------------- smem layout
@@ -219,7 +225,7 @@ __device__ __forceinline__ void zero_smem(unsigned char *smem, int from, int to)
 // Histogram this CTA's slice, then push the per-expert partial (and the CTA's
 // min bad pair index) into row `rank` of every CTA's partial table.  Ends with
 // the cluster barrier; afterwards part[r][e] holds CTA r's count of expert e.
-template <bool PRIV>
+template <bool PRIV, bool COUNT = true>
 __device__ void histogram_push(const Params &p, const Layout &L, unsigned char *smem, int64_t beg, int n_local,
                                uint32_t R, uint32_t rank) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -230,7 +236,9 @@ __device__ void histogram_push(const Params &p, const Layout &L, unsigned char *
     const int32_t *src = p.staged ? reinterpret_cast<const int32_t *>(smem + L.ids) : (p.ids + beg);
     int64_t my_bad = kNoBad;
 
-    if (!PRIV) {
+    if (!COUNT) {
+        // the gating stage already counted its ids into hist (gate_topk)
+    } else if (!PRIV) {
         const int cm = p.C - 1;
         const int n4 = n_local & ~3;
         const bool vec = p.staged || ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
@@ -888,7 +896,96 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
 }
 
 // ================================================================ kernels
-template <int W, bool PRIV>
+
+// ---------------------------------------------------------------- gating top-k (fused)
+// Order key of an fp32 score: unsigned compare == float compare (NaN excluded).
+__device__ __forceinline__ uint32_t okey(float f) {
+    const uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+// Top-k of every token of this CTA's slice, fused with the histogram: one warp per
+// token, two tokens in flight per warp (one for N > 256).  Lane l holds experts l + 32 j as 64-bit
+// keys (score key << 32 | ~expert), sorted descending in registers (bitonic
+// network), so "largest score, then lowest expert id" is the u64 max.  Round r: two
+// redux.sync (max of the high words, then of the low words among the lanes holding
+// that maximum) name the winner; its owner lane pops its head.  Ids are written in
+// descending score order (core.py:322-326), staged in shared memory for the
+// routing phases and counted into the lane-striped histogram.
+template <int NPL>
+__device__ __forceinline__ void lane_sort_desc(uint64_t (&c)[NPL]) {
+#pragma unroll
+    for (int size = 2; size <= NPL; size <<= 1)
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1)
+#pragma unroll
+            for (int i = 0; i < NPL; ++i) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool desc = ((i & size) == 0);
+                    const uint64_t a = c[i], b = c[j];
+                    const bool sw = desc ? (a < b) : (a > b);
+                    c[i] = sw ? b : a;
+                    c[j] = sw ? a : b;
+                }
+            }
+}
+
+template <int NPL>
+__device__ void gate_topk(const Params &p, const Layout &L, unsigned char *smem, int64_t tok_beg, int n_tok) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int N = p.N, k = p.top_k, cm = p.C - 1;
+    int32_t *s_ids = reinterpret_cast<int32_t *>(smem + L.ids);
+    int32_t *s_hist = reinterpret_cast<int32_t *>(smem + L.hist);
+    constexpr int TPW = NPL <= 8 ? 2 : 1;  // tokens in flight per warp (register budget)
+    for (int t0 = TPW * warp; t0 < n_tok; t0 += TPW * kWarps) {
+        const bool two = TPW == 2 && t0 + 1 < n_tok;
+        uint64_t c[TPW][NPL];
+#pragma unroll
+        for (int q = 0; q < TPW; ++q) {
+            const float *row = p.scores + (tok_beg + t0 + (q && two ? 1 : 0)) * static_cast<int64_t>(N);
+#pragma unroll
+            for (int j = 0; j < NPL; ++j) {
+                const int e = lane + 32 * j;
+                c[q][j] = (e < N) ? ((static_cast<uint64_t>(okey(__ldg(row + e))) << 32) |
+                                     static_cast<uint64_t>(0xffffffffu - static_cast<uint32_t>(e)))
+                                  : 0ull;
+            }
+            lane_sort_desc<NPL>(c[q]);
+        }
+        int mine[TPW];
+#pragma unroll
+        for (int q = 0; q < TPW; ++q) mine[q] = 0;
+        for (int r = 0; r < k; ++r) {
+#pragma unroll
+            for (int q = 0; q < TPW; ++q) {
+                const uint32_t hi = static_cast<uint32_t>(c[q][0] >> 32);
+                const uint32_t mh = __reduce_max_sync(kFull, hi);
+                const uint32_t lo = (hi == mh) ? static_cast<uint32_t>(c[q][0]) : 0u;
+                const uint32_t ml = __reduce_max_sync(kFull, lo);
+                const int e = static_cast<int>(0xffffffffu - ml);
+                if ((e & 31) == lane) {
+#pragma unroll
+                    for (int j = 0; j + 1 < NPL; ++j) c[q][j] = c[q][j + 1];
+                    c[q][NPL - 1] = 0ull;
+                }
+                if (lane == r) mine[q] = e;
+            }
+        }
+        if (lane < k) {
+#pragma unroll
+            for (int q = 0; q < TPW; ++q) {
+                if (q == 1 && !two) break;
+                const int tl = t0 + q;
+                const int e = mine[q];
+                s_ids[tl * k + lane] = e;
+                p.ids_out[(tok_beg + tl) * k + lane] = e;
+                atomicAdd(&s_hist[e * p.C + (lane & cm)], 1);
+            }
+        }
+    }
+}
+
+template <int W, bool PRIV, int GATE_NPL = 0>
 __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t R = cluster_nctarank(), rank = cluster_ctarank();
@@ -896,18 +993,25 @@ __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) 
     const int64_t beg = static_cast<int64_t>(rank) * p.slice;
     const int64_t rem_pairs = p.num_pairs - beg;
     const int n_local = rem_pairs <= 0 ? 0 : static_cast<int>(rem_pairs < p.slice ? rem_pairs : p.slice);
-    const StagePlan sp = stage_plan<W>(p, beg, n_local, p.staged != 0);
+    constexpr bool GATE = GATE_NPL > 0;
+    const StagePlan sp = stage_plan<W>(p, beg, n_local, !GATE && p.staged != 0);
     if (threadIdx.x == 0) stage_issue(p, L, smem, beg, sp);
     if (R > 1) cluster_arrive_release();  // after thread 0 initialised the mbarriers
     stamp(p, 0);
     int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
     init_misc(misc);
     zero_smem(smem, L.aux, L.part);  // forced counts + histogram
-    stage_rest(p, L, smem, beg, n_local, p.staged != 0, sp);
+    stage_rest(p, L, smem, beg, n_local, !GATE && p.staged != 0, sp);
     __syncthreads();
+    if (GATE) {
+        // the slice is whole tokens: slice = tokens per CTA * top_k
+        const int64_t tok_beg = beg / p.top_k;
+        gate_topk<(GATE ? GATE_NPL : 1)>(p, L, smem, tok_beg, n_local / p.top_k);
+        __syncthreads();
+    }
     mbar_wait(reinterpret_cast<uint64_t *>(smem + L.mbar), 0);
     stamp(p, 1);
-    histogram_push<PRIV>(p, L, smem, beg, n_local, R, rank);
+    histogram_push<PRIV, !GATE>(p, L, smem, beg, n_local, R, rank);
     const bool writer = (rank == 0);
     if (!p.mask) {  // aggregate_loads only (core.py:236-244)
         bad_min_warp0(L, smem, R, p.N);
@@ -1404,6 +1508,58 @@ int metro_route_v1(const int32_t *ids, int64_t num_pairs, const uint32_t *mask, 
         METRO_DISPATCH_W(W, return launch(metro_ids_kernel<kW, false>, R, smem, s, p));
     }
     return METRO_EDIMS;
+}
+
+// Gating mode: plan like plan_ids, but every CTA's slice is whole tokens.
+static int plan_gate(int64_t num_tokens, int k, int N, int requested, Params &p, int &R) {
+    int cands[8], nc = 0;
+    if (requested > 0) {
+        if (requested != 1 && requested != 2 && requested != 4 && requested != 8 && requested != 16)
+            return METRO_EARG;
+        cands[nc++] = requested;
+    } else {
+        for (int r = auto_cluster(num_tokens * k); r >= 1; r >>= 1) cands[nc++] = r;
+    }
+    for (int ci = 0; ci < nc; ++ci) {
+        const int r = cands[ci];
+        const int64_t tpc = (num_tokens + r - 1) / r;
+        const int64_t slice = tpc * k > 0 ? tpc * k : k;
+        if (slice > INT32_MAX / 8) continue;
+        for (int C = copies_for(N); C >= 1; C >>= 1) {
+            const Layout L = make_layout(kMetroIds, N, 1, r, slice, C, 1, false);
+            if (L.total <= kMaxSmem) {
+                p.slice = slice;
+                p.staged = 1;
+                p.C = C;
+                R = r;
+                return L.total;
+            }
+        }
+    }
+    return METRO_EDIMS;
+}
+
+int metro_route_scores_v1(const float *scores, int64_t num_tokens, int32_t top_k, const uint32_t *mask, int32_t N,
+                          int32_t G, int32_t *topk_ids, int32_t *loads, int32_t *choice, int32_t *rank_counts,
+                          int32_t *lam, int32_t *pair_rank, int32_t *status, int32_t cluster_ctas, void *stream) {
+    if ((!scores && num_tokens > 0) || (!topk_ids && num_tokens > 0) || !mask || !choice || !rank_counts ||
+        !lam || !status || num_tokens < 0 || top_k < 1)
+        return METRO_EARG;
+    int rc = check_dims(N, G);
+    if (rc) return rc;
+    if (G > 32 || N > 512 || top_k > 32 || top_k > N) return METRO_EDIMS;
+    Params p = {};
+    p.scores = scores; p.num_tokens = num_tokens; p.top_k = top_k; p.ids_out = topk_ids;
+    p.num_pairs = num_tokens * top_k; p.mask = mask; p.N = N; p.G = G;
+    p.loads = loads; p.choice = choice; p.rank_counts = rank_counts; p.lam = lam;
+    p.pair_rank = pair_rank; p.status = status; p.stamps = g_stamps;
+    int R = 1;
+    const int smem = plan_gate(num_tokens, top_k, N, cluster_ctas, p, R);
+    if (smem < 0) return smem;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (N <= 128) return launch(metro_ids_kernel<1, false, 4>, R, smem, s, p);
+    if (N <= 256) return launch(metro_ids_kernel<1, false, 8>, R, smem, s, p);
+    return launch(metro_ids_kernel<1, false, 16>, R, smem, s, p);
 }
 
 int metro_aggregate_loads_v1(const int32_t *ids, int64_t num_pairs, int32_t N, int32_t *loads,

@@ -186,6 +186,38 @@ class Router:
         return out
 
 
+    def route_scores(self, scores: torch.Tensor, top_k: int, out: Optional[RouteResult] = None,
+                     topk_ids: Optional[torch.Tensor] = None, pair_rank: bool = True,
+                     stream: Optional[torch.cuda.Stream] = None):
+        """Gating top-k fused with METRO (metro_route_scores_v1): ``scores`` fp32
+        [B, N] router scores of the all-gathered tokens -> (topk_ids int32 [B, k],
+        RouteResult).  Each token's ids are its k largest scores, largest first,
+        ties to the lower expert id (the reference generator's order,
+        core.py:319-326)."""
+        if self.kind != "metro":
+            raise ValidationError("route_scores is the METRO router's fused gating entry point")
+        p = self.placement
+        if scores.dtype != torch.float32 or scores.dim() != 2 or not scores.is_cuda or not scores.is_contiguous():
+            raise ValidationError("scores must be a contiguous float32 CUDA tensor [tokens, experts]")
+        if scores.device != p.device:
+            raise ValidationError(f"scores on {scores.device}, placement on {p.device}")
+        B, n = scores.shape
+        if n != p.num_experts:
+            raise ValidationError(f"dimension mismatch: scores have {n} experts, A has {p.num_experts}")
+        k = int(top_k)
+        if topk_ids is None:
+            topk_ids = torch.empty((B, k), dtype=torch.int32, device=p.device)
+        if out is None:
+            out = self.alloc(B * k, pair_rank=pair_rank, top_k=k)
+        s = _stream(p.device, stream)
+        rc = _native.lib().metro_route_scores_v1(
+            scores.data_ptr(), B, k, p.mask.data_ptr(), p.num_experts, p.num_ranks, topk_ids.data_ptr(),
+            _ptr(out.loads), out.choice.data_ptr(), out.rank_counts.data_ptr(), out.lam.data_ptr(),
+            _ptr(out.pair_rank), out.status.data_ptr(), self.cluster_ctas, s)
+        _native.check_rc(rc, "metro_route_scores_v1")
+        return topk_ids, out
+
+
 def aggregate_loads_device(topk_ids: torch.Tensor, num_experts: int, cluster_ctas: int = 0,
                            stream: Optional[torch.cuda.Stream] = None):
     """T[N] int32 on device + status[4] (metro_aggregate_loads_v1)."""

@@ -24,6 +24,12 @@ Fixtures
                  with METRO and EPLB outputs.
 ``placement.npz`` zipf_popularity / eplb_replicate / eplb_place outputs used to pin
                  the package's cold-path placement + synthetic-trace generator.
+``gate.npz``     the gating scores behind gen_zipf_trace's top-k (core.py:316-326:
+                 log(popularity) + Gumbel noise from the same seeded stream), as
+                 float32, with the reference's top-k ids for the same batch -- pins
+                 the fused gating top-k (metro_route_scores_v1) and its oracle.
+
+``python make_golden.py gate`` rewrites gate.npz only.
 """
 
 from __future__ import annotations
@@ -207,7 +213,39 @@ def make_placement_golden() -> dict:
     return out
 
 
+GATE_CASES = [  # (N, k, G, tokens per GPU, skew, seed)
+    (128, 8, 8, 32, 1.2, 1000),   # Qwen3-30B-A3B, B=256
+    (256, 8, 8, 32, 1.2, 1000),   # DeepSeek-V3, B=256
+    (256, 8, 8, 8, 0.5, 1001),    # DeepSeek-V3, flatter popularity
+    (512, 8, 8, 8, 1.2, 1002),    # N at the kernel limit
+    (64, 1, 4, 16, 1.2, 1003),    # top-1
+    (64, 32, 4, 4, 2.0, 1004),    # top-32, strong skew
+]
+
+
+def make_gate() -> dict:
+    out = {}
+    for j, (n, k, g, tpg, skew, seed) in enumerate(GATE_CASES):
+        batch = gen_zipf_trace(model(n, k), cluster(g), tpg, skew, seed, popularity_seed=HISTORY_SEED)
+        ids = np.array([t.expert_ids for t in batch.tokens], dtype=np.int32).reshape(-1, k)
+        # the same scores the generator ranks (core.py:316-322, same seeded stream)
+        probs = zipf_popularity(n, skew, HISTORY_SEED)
+        rng = np.random.default_rng(seed)
+        keys = np.log(probs)[None, :] + rng.gumbel(size=(tpg * g, n))
+        assert (np.argsort(-keys, axis=1, kind="stable")[:, :k] == ids).all()
+        out[f"g{j}_meta"] = np.array([n, k, g, tpg * g, seed], dtype=np.int64)
+        out[f"g{j}_scores"] = keys.astype(np.float32)
+        out[f"g{j}_ids"] = ids
+    out["count"] = np.array(len(GATE_CASES))
+    return out
+
+
 def main() -> None:
+    if sys.argv[1:] == ["gate"]:
+        np.savez_compressed(os.path.join(HERE, "gate.npz"), **make_gate())
+        print("wrote gate.npz")
+        return
+    np.savez_compressed(os.path.join(HERE, "gate.npz"), **make_gate())
     np.savez_compressed(os.path.join(HERE, "shapes.npz"), **make_shapes())
     np.savez_compressed(os.path.join(HERE, "small.npz"), **make_small())
     np.savez_compressed(os.path.join(HERE, "placement.npz"), **make_placement_golden())

@@ -1,0 +1,104 @@
+"""Gating top-k fused with METRO routing (metro_route_scores_v1).
+
+CPU: the oracle's top-k over the float32 gating scores reproduces the reference
+generator's top-k ids (core.py:319-326) on every golden case.  GPU (-m gpu): the
+fused kernel's ids equal the oracle's, and its routing outputs equal the oracle
+routing of those ids -- golden cases at every cluster size, random scores with
+forced ties (tie -> lower expert id), limits and argument errors.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2512_09277_b200 import DevicePlacement, Router, ValidationError
+from paper_2512_09277_b200.placement import make_placement
+
+
+def test_oracle_topk_matches_reference_generator(gate):
+    for c in gate:
+        assert (oracle.gate_topk(c["scores"], c["k"]) == c["ids"]).all(), (c["N"], c["k"])
+
+
+def test_oracle_topk_ties_lower_id():
+    sc = np.array([[1, 3, 3, 2, 3]], np.float32)
+    assert oracle.gate_topk(sc, 4).tolist() == [[1, 2, 4, 3]]
+
+
+@pytest.fixture(scope="module")
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    torch.cuda.init()
+
+
+def _fused(scores, k, A, cluster=0):
+    pl = DevicePlacement(A)
+    r = Router(pl, "metro", cluster)
+    st = torch.from_numpy(np.ascontiguousarray(scores, np.float32)).cuda()
+    ids, out = r.route_scores(st, k)
+    out.check()
+    return ids.cpu().numpy(), out
+
+
+def _check_routing(ids, out, A):
+    loads = oracle.aggregate_loads(ids, A.shape[0])
+    choice, counts, lam = oracle.route_metro(loads, A)
+    assert (out.loads.cpu().numpy() == loads).all()
+    assert (out.choice.cpu().numpy() == choice).all()
+    assert (out.rank_counts.cpu().numpy() == counts).all()
+    assert int(out.lam.item()) == lam
+    pr = oracle.pair_rank_metro(ids, choice)
+    assert (out.pair_rank.cpu().numpy() == pr.reshape(-1)).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cluster", [0, 1, 2, 4, 8, 16])
+def test_fused_gate_golden(_cuda, gate, cluster):
+    for c in gate:
+        A = make_placement(c["N"], c["G"], 1.5, 7).matrix
+        ids, out = _fused(c["scores"], c["k"], A, cluster)
+        assert (ids == c["ids"]).all(), (c["N"], c["k"], cluster)
+        _check_routing(ids, out, A)
+
+
+@pytest.mark.gpu
+def test_fused_gate_random_with_ties(_cuda):
+    rng = np.random.default_rng(9)
+    for it in range(60):
+        n = int(rng.choice([8, 33, 64, 100, 128, 200, 256, 300, 512]))
+        g = int(rng.choice([2, 4, 8, 16, 32]))
+        k = int(rng.integers(1, min(32, n) + 1))
+        B = int(rng.integers(0, 1500))
+        A = (rng.random((n, g)) < 2.0 / g).astype(np.int8)
+        A[np.arange(n), rng.integers(0, g, n)] = 1
+        if it % 3 == 0:  # heavy ties: small integer scores (incl. negatives)
+            sc = rng.integers(-3, 4, size=(B, n)).astype(np.float32)
+        else:
+            sc = rng.standard_normal((B, n)).astype(np.float32)
+        ids, out = _fused(sc, k, A, int(rng.choice([0, 1, 4, 16])))
+        ref = oracle.gate_topk(sc, k) if B else np.zeros((0, k), np.int32)
+        assert (ids == ref).all(), it
+        if B:
+            _check_routing(ids, out, A)
+
+
+@pytest.mark.gpu
+def test_fused_gate_limits_and_errors(_cuda):
+    A = make_placement(256, 8, 1.5, 7).matrix
+    sc = np.random.default_rng(1).standard_normal((4096, 256)).astype(np.float32)
+    ids, out = _fused(sc, 8, A)
+    assert (ids == oracle.gate_topk(sc, 8)).all()
+    _check_routing(ids, out, A)
+    pl = DevicePlacement(A)
+    r = Router(pl, "metro")
+    with pytest.raises(ValidationError):
+        r.route_scores(torch.zeros((4, 255), device="cuda"), 8)  # dimension mismatch
+    with pytest.raises(ValidationError):
+        r.route_scores(torch.zeros((4, 256), device="cuda"), 33)  # k > 32
+    with pytest.raises(ValidationError):
+        r.route_scores(torch.zeros((4, 256), device="cuda", dtype=torch.float64), 8)
+    big = DevicePlacement(np.ones((600, 8), np.int8))
+    with pytest.raises(ValidationError):
+        Router(big, "metro").route_scores(torch.zeros((4, 600), device="cuda"), 8)  # N > 512
