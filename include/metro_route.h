@@ -114,13 +114,22 @@ METRO_API int metro_route_v1(const int32_t *topk_ids, int64_t num_pairs, const u
  * largest score first, ties to the lower expert id, the descending-key order of
  * the reference's generator (core.py:319-326) -- are written to topk_ids
  * [num_tokens, top_k] and routed in the same launch (no separate pass over the
- * ids).  Other outputs as metro_route_v1.  Limits: N <= 512, G <= 32,
- * top_k <= 32, top_k <= N; NaN scores are not supported. */
+ * ids).  Other outputs as metro_route_v1.
+ * ws: metro_scores_workspace_bytes(N) bytes of device memory, ZEROED ONCE by the
+ * caller; the kernel leaves it zeroed (one workspace per stream).  Two variants:
+ *   whole GPU   -- 32 tokens' top-k per CTA on every SM, partial counts added into
+ *                  ws with atomics, the last CTA to finish routes (needs ws);
+ *   one cluster -- the routing cluster also takes the top-k (no ws needed).
+ * cluster_ctas: 0 = auto (one cluster up to 512 tokens, whole GPU above when ws
+ * is given), -1 = whole GPU, 1/2/4/8/16 = one cluster of that size.
+ * Limits: N <= 512, G <= 32, top_k <= 32, top_k <= N; NaN scores are
+ * not supported. */
+METRO_API size_t metro_scores_workspace_bytes(int32_t num_experts);
 METRO_API int metro_route_scores_v1(const float *scores, int64_t num_tokens, int32_t top_k,
                                     const uint32_t *rank_mask, int32_t num_experts, int32_t num_ranks,
                                     int32_t *topk_ids, int32_t *loads, int32_t *choice, int32_t *rank_counts,
-                                    int32_t *lam, int32_t *pair_rank, int32_t *status, int32_t cluster_ctas,
-                                    void *stream);
+                                    int32_t *lam, int32_t *pair_rank, int32_t *status, void *ws,
+                                    int32_t cluster_ctas, void *stream);
 
 /* aggregate_loads only (core.py:236-244): loads[N] from the ids; status as above. */
 METRO_API int metro_aggregate_loads_v1(const int32_t *topk_ids, int64_t num_pairs,

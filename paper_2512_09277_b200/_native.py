@@ -69,7 +69,8 @@ def lib() -> ctypes.CDLL:
         "metro_pack_placement": ([P, i32, i32, P], ctypes.c_int),
         "metro_aggregate_loads_v1": ([P, i64, i32, P, P, i32, P], ctypes.c_int),
         "metro_route_v1": ([P, i64, P, i32, i32, P, P, P, P, P, P, i32, P], ctypes.c_int),
-        "metro_route_scores_v1": ([P, i64, i32, P, i32, i32, P, P, P, P, P, P, P, i32, P], ctypes.c_int),
+        "metro_route_scores_v1": ([P, i64, i32, P, i32, i32, P, P, P, P, P, P, P, P, i32, P], ctypes.c_int),
+        "metro_scores_workspace_bytes": ([i32], ctypes.c_size_t),
         "metro_route_from_loads_v1": ([P, P, i32, i32, P, P, P, P, P], ctypes.c_int),
         "metro_route_ordered_v1": ([P, i32, P, i32, i32, P, P, P, P, P], ctypes.c_int),
         "eplb_route_v1": ([P, i64, P, i32, i32, P, P, P, P, P, P, i32, P], ctypes.c_int),

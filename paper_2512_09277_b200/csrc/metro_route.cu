@@ -79,14 +79,20 @@ struct Params {
     int64_t num_tokens;
     int32_t top_k;
     int32_t *ids_out;
+    int32_t score_bytes;  // > 0: the CTA's score rows are staged in smem (bytes per CTA)
+    void *gate_ws;        // metro_gate_kernel: int64 T[N] + arrival counter, zero between launches
 };
+constexpr int kGateTokens = 2 * kThreads / 32;  // tokens per CTA in metro_gate_kernel
+// auto policy of metro_route_scores_v1: above this many tokens the whole GPU takes
+// the top-k (measured crossover on B200: ~600 tokens at N = 256)
+constexpr int64_t kGateWholeGpuMin = 512;
 
 // ---------------------------------------------------------------- smem layout
 // mbar | misc | mask | ids (staged slice) | T | choice | aux | hist | part
 // The METRO sort/greedy scratch (keys, cand, smask, sid) aliases hist + part:
 // both are dead once the partial histograms have been reduced into T.
 struct Layout {
-    int mbar, misc, mask, ids, T, choice, aux, hist, part, keys, cand, smask, sid, ent, rpart, total;
+    int mbar, misc, mask, ids, T, choice, aux, hist, part, keys, cand, smask, sid, ent, rpart, sc, total;
     int NP;  // partial-row stride (words): N + 2 (bad pair lo/hi) rounded to 4
 };
 
@@ -96,7 +102,7 @@ __host__ __device__ inline int align_up(int x, int a) { return (x + a - 1) / a *
 constexpr int kES = 12;  // packed greedy entry stride (words)
 
 __host__ __device__ inline Layout make_layout(int kind, int N, int W, int R, int64_t slice,
-                                              int C, int staged, bool warp_hist = false) {
+                                              int C, int staged, bool warp_hist = false, int score_bytes = 0) {
     Layout L;
     int o = 0;
     L.mbar = o; o += 16;
@@ -125,6 +131,9 @@ __host__ __device__ inline Layout make_layout(int kind, int N, int W, int R, int
     L.rpart = align_up(L.ent + (W == 1 ? (N + 16) * kES * 4 : 0), 16);  // [4][N] partial ranks
     const int end2 = metro ? align_up(L.rpart + (4 * N + 16) * 4, 16) : o;  // + prefetch slack
     L.total = end1 > end2 ? end1 : end2;
+    // gating mode: the CTA's fp32 score rows, staged by TMA bulk copies
+    L.sc = align_up(L.total, 128);
+    if (score_bytes > 0) L.total = L.sc + score_bytes;
     return L;
 }
 
@@ -187,10 +196,22 @@ __device__ __forceinline__ void stage_issue(const Params &p, const Layout &L, un
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + L.mbar);
     mbar_init(bar + 1, 1);  // partial-histogram exchange (st.async from the peer CTAs)
     mbar_init(bar, 1);      // TMA staging (its init fence covers both)
-    const uint32_t bytes = (s.mask_bulk ? s.mask_words * 4u : 0u) + (s.ids_bulk ? s.body * 4u : 0u);
+    uint32_t sc_bytes = 0;
+    const float *sc_src = nullptr;
+    if (p.score_bytes > 0) {  // gating mode: this CTA's rows of the score matrix
+        const int64_t t0 = beg / p.top_k;
+        const int64_t nt = min(static_cast<int64_t>(p.slice / p.top_k), p.num_tokens - t0);
+        sc_bytes = nt > 0 ? static_cast<uint32_t>(nt * p.N * 4) : 0u;
+        sc_src = p.scores + t0 * p.N;
+    }
+    const uint32_t bytes = (s.mask_bulk ? s.mask_words * 4u : 0u) + (s.ids_bulk ? s.body * 4u : 0u) + sc_bytes;
     mbar_arrive_expect_tx(bar, bytes);
     if (s.mask_bulk) bulk_g2s(smem + L.mask, p.mask, s.mask_words * 4u, bar);
     if (s.ids_bulk) bulk_g2s(smem + L.ids, p.ids + beg, s.body * 4u, bar);
+    for (uint32_t o = 0; o < sc_bytes; o += 32768u) {
+        const uint32_t n = min(32768u, sc_bytes - o);
+        bulk_g2s(smem + L.sc + o, reinterpret_cast<const unsigned char *>(sc_src) + o, n, bar);
+    }
 }
 
 // all threads: whatever the TMA could not take (unaligned / ragged tail)
@@ -930,23 +951,26 @@ __device__ __forceinline__ void lane_sort_desc(uint64_t (&c)[NPL]) {
             }
 }
 
+// s_ids == nullptr: ids go to global memory only; hist[e * C + lane % C] counts.
 template <int NPL>
-__device__ void gate_topk(const Params &p, const Layout &L, unsigned char *smem, int64_t tok_beg, int n_tok) {
+__device__ void gate_topk(const Params &p, const Layout &L, unsigned char *smem, int64_t tok_beg, int n_tok,
+                          int32_t *s_ids, int32_t *s_hist, int C) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int N = p.N, k = p.top_k, cm = p.C - 1;
-    int32_t *s_ids = reinterpret_cast<int32_t *>(smem + L.ids);
-    int32_t *s_hist = reinterpret_cast<int32_t *>(smem + L.hist);
+    const int N = p.N, k = p.top_k, cm = C - 1;
     constexpr int TPW = NPL <= 8 ? 2 : 1;  // tokens in flight per warp (register budget)
     for (int t0 = TPW * warp; t0 < n_tok; t0 += TPW * kWarps) {
         const bool two = TPW == 2 && t0 + 1 < n_tok;
         uint64_t c[TPW][NPL];
 #pragma unroll
         for (int q = 0; q < TPW; ++q) {
-            const float *row = p.scores + (tok_beg + t0 + (q && two ? 1 : 0)) * static_cast<int64_t>(N);
+            const int tq = t0 + (q && two ? 1 : 0);
+            const float *row = p.score_bytes > 0
+                                   ? reinterpret_cast<const float *>(smem + L.sc) + static_cast<int64_t>(tq) * N
+                                   : p.scores + (tok_beg + tq) * static_cast<int64_t>(N);
 #pragma unroll
             for (int j = 0; j < NPL; ++j) {
                 const int e = lane + 32 * j;
-                c[q][j] = (e < N) ? ((static_cast<uint64_t>(okey(__ldg(row + e))) << 32) |
+                c[q][j] = (e < N) ? ((static_cast<uint64_t>(okey(row[e])) << 32) |
                                      static_cast<uint64_t>(0xffffffffu - static_cast<uint32_t>(e)))
                                   : 0ull;
             }
@@ -977,9 +1001,9 @@ __device__ void gate_topk(const Params &p, const Layout &L, unsigned char *smem,
                 if (q == 1 && !two) break;
                 const int tl = t0 + q;
                 const int e = mine[q];
-                s_ids[tl * k + lane] = e;
+                if (s_ids) s_ids[tl * k + lane] = e;
                 p.ids_out[(tok_beg + tl) * k + lane] = e;
-                atomicAdd(&s_hist[e * p.C + (lane & cm)], 1);
+                atomicAdd(&s_hist[e * C + (lane & cm)], 1);
             }
         }
     }
@@ -989,7 +1013,7 @@ template <int W, bool PRIV, int GATE_NPL = 0>
 __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t R = cluster_nctarank(), rank = cluster_ctarank();
-    const Layout L = make_layout(kMetroIds, p.N, W, R, p.slice, p.C, p.staged, PRIV);
+    const Layout L = make_layout(kMetroIds, p.N, W, R, p.slice, p.C, p.staged, PRIV, p.score_bytes);
     const int64_t beg = static_cast<int64_t>(rank) * p.slice;
     const int64_t rem_pairs = p.num_pairs - beg;
     const int n_local = rem_pairs <= 0 ? 0 : static_cast<int>(rem_pairs < p.slice ? rem_pairs : p.slice);
@@ -1006,7 +1030,10 @@ __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) 
     if (GATE) {
         // the slice is whole tokens: slice = tokens per CTA * top_k
         const int64_t tok_beg = beg / p.top_k;
-        gate_topk<(GATE ? GATE_NPL : 1)>(p, L, smem, tok_beg, n_local / p.top_k);
+        if (p.score_bytes > 0) mbar_wait(reinterpret_cast<uint64_t *>(smem + L.mbar), 0);
+        gate_topk<(GATE ? GATE_NPL : 1)>(p, L, smem, tok_beg, n_local / p.top_k,
+                                         reinterpret_cast<int32_t *>(smem + L.ids),
+                                         reinterpret_cast<int32_t *>(smem + L.hist), p.C);
         __syncthreads();
     }
     mbar_wait(reinterpret_cast<uint64_t *>(smem + L.mbar), 0);
@@ -1080,6 +1107,92 @@ __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) 
         }
     }
     stamp(p, 7);
+}
+
+// Gating top-k + METRO across the whole GPU in one launch (metro_route_scores_v1).
+// Every CTA takes top-k for 32 tokens (2 per warp), writes their ids and adds its
+// shared histogram into the int64 workspace T with global atomics; the last CTA
+// to finish (threadfence + arrival counter, no grid-wide barrier) routes from T
+// with the single-CTA decide path, writes every pair's rank, and re-zeroes the
+// workspace for the next launch.
+template <int W, int NPL>
+__global__ void __launch_bounds__(kThreads, 1) metro_gate_kernel(const Params p) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const Layout L = make_layout(kMetroLoads, p.N, W, 1, 0, 1, 0);
+    const int tid = threadIdx.x, N = p.N, k = p.top_k;
+    // every CTA stages the rank masks (1 KB) right away: whichever CTA ends up
+    // routing already has them
+    const StagePlan sp = stage_plan<W>(p, 0, 0, false);
+    if (tid == 0) stage_issue(p, L, smem, 0, sp);
+    int32_t *s_hist = reinterpret_cast<int32_t *>(smem + L.keys);  // decide scratch, free here
+    int32_t &s_last = reinterpret_cast<int32_t *>(smem + L.misc)[63];  // misc is initialised later
+    for (int e = tid; e < N; e += kThreads) s_hist[e] = 0;
+    __syncthreads();
+    const int64_t tok_beg = static_cast<int64_t>(blockIdx.x) * kGateTokens;
+    const int64_t rem = p.num_tokens - tok_beg;
+    const int n_tok = rem <= 0 ? 0 : static_cast<int>(rem < kGateTokens ? rem : kGateTokens);
+    gate_topk<NPL>(p, L, smem, tok_beg, n_tok, nullptr, s_hist, 1);
+    __syncthreads();
+    unsigned long long *wsT = reinterpret_cast<unsigned long long *>(p.gate_ws);
+    for (int e = tid; e < N; e += kThreads)
+        if (s_hist[e]) atomicAdd(wsT + e, static_cast<unsigned long long>(s_hist[e]));
+    __threadfence();
+    __syncthreads();
+    unsigned int *arrived = reinterpret_cast<unsigned int *>(wsT + N);
+    if (tid == 0) s_last = (atomicAdd(arrived, 1u) == gridDim.x - 1);
+    stage_rest(p, L, smem, 0, 0, false, sp);
+    __syncthreads();
+    const bool last = s_last != 0;
+    mbar_wait(reinterpret_cast<uint64_t *>(smem + L.mbar), 0);  // no CTA exits with a copy in flight
+    __syncthreads();  // misc (s_last's home) is re-initialised below
+    if (!last) return;
+    __threadfence();  // every other CTA's ids and counts are visible from here on
+
+    // ---- last CTA: METRO from T (routing.py:105-113), then every pair's rank
+    init_misc(reinterpret_cast<int32_t *>(smem + L.misc));
+    zero_smem(smem, L.aux, L.hist);
+    __syncthreads();
+    Params q = p;
+    q.loads_in = reinterpret_cast<const int64_t *>(p.gate_ws);
+    const bool ok = metro_decide<W, kFromLoads>(q, L, smem, true, 1, 0);
+    __syncthreads();
+    for (int e = tid; e < N; e += kThreads) {  // loads out; workspace reset for the next launch
+        if (p.loads) p.loads[e] = static_cast<int32_t>(__ldcg(reinterpret_cast<const long long *>(wsT) + e));
+        wsT[e] = 0ull;
+    }
+    if (tid == 0) *arrived = 0u;
+    if (!ok) return;
+    const int32_t *s_choice = reinterpret_cast<const int32_t *>(smem + L.choice);
+    for (int e = tid; e < N; e += kThreads) p.choice[e] = s_choice[e];
+    if (p.pair_rank) {
+        // ids from L2 (written by the other CTAs): 16-byte loads, four in flight
+        const int64_t np = p.num_tokens * k;
+        const int64_t n4 = ((reinterpret_cast<uintptr_t>(p.ids_out) | reinterpret_cast<uintptr_t>(p.pair_rank)) & 15)
+                               ? 0 : (np >> 2);
+        const int4 *src4 = reinterpret_cast<const int4 *>(p.ids_out);
+        int4 *dst4 = reinterpret_cast<int4 *>(p.pair_rank);
+        constexpr int U = 4;
+        for (int64_t i0 = tid; i0 < n4; i0 += static_cast<int64_t>(kThreads) * U) {
+            int4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t i = i0 + static_cast<int64_t>(u) * kThreads;
+                v[u] = (i < n4) ? __ldcg(src4 + i) : make_int4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t i = i0 + static_cast<int64_t>(u) * kThreads;
+                if (i < n4)
+                    dst4[i] = make_int4(s_choice[v[u].x], s_choice[v[u].y], s_choice[v[u].z], s_choice[v[u].w]);
+            }
+        }
+        for (int64_t i = n4 * 4 + tid; i < np; i += kThreads) p.pair_rank[i] = s_choice[__ldcg(p.ids_out + i)];
+    }
+    if (tid == 0) {
+        p.status[0] = METRO_OK;
+        p.status[1] = p.status[2] = 0;
+        p.status[3] = static_cast<int32_t>(gridDim.x);
+    }
 }
 
 // METRO from loads (compat route_metro(T, A)) or from a caller order (metro-parallel).
@@ -1362,6 +1475,15 @@ static int launch(K kernel, int R, int smem, cudaStream_t s, Args... args) {
     return METRO_OK;
 }
 
+// ordinary (non-cluster) grid launch
+template <typename K, typename... Args>
+static cudaError_t launch_plain(K kernel, int grid, int smem, cudaStream_t s, Args... args) {
+    cudaError_t e = prepare(kernel);
+    if (e != cudaSuccess) return e;
+    kernel<<<grid, kThreads, smem, s>>>(args...);
+    return cudaGetLastError();
+}
+
 static int words_for(int G) { return (G + 31) / 32; }
 static int copies_for(int N) {
     static const int forced = [] {  // tuning override (power of two 1..32)
@@ -1518,30 +1640,44 @@ static int plan_gate(int64_t num_tokens, int k, int N, int requested, Params &p,
             return METRO_EARG;
         cands[nc++] = requested;
     } else {
-        for (int r = auto_cluster(num_tokens * k); r >= 1; r >>= 1) cands[nc++] = r;
+        // the top-k is the heavy part here: about 8 tokens per CTA (measured on B200:
+        // 4..16 CTAs for 64..512 tokens), at least 4 CTAs
+        int r0 = 4;
+        while (r0 < kMaxCluster && num_tokens > static_cast<int64_t>(r0) * 8) r0 *= 2;
+        for (int r = r0; r >= 1; r >>= 1) cands[nc++] = r;
     }
     for (int ci = 0; ci < nc; ++ci) {
         const int r = cands[ci];
         const int64_t tpc = (num_tokens + r - 1) / r;
         const int64_t slice = tpc * k > 0 ? tpc * k : k;
         if (slice > INT32_MAX / 8) continue;
-        for (int C = copies_for(N); C >= 1; C >>= 1) {
-            const Layout L = make_layout(kMetroIds, N, 1, r, slice, C, 1, false);
-            if (L.total <= kMaxSmem) {
-                p.slice = slice;
-                p.staged = 1;
-                p.C = C;
-                R = r;
-                return L.total;
+        // staged score rows need 16-byte rows for the bulk copies
+        const bool can_stage = (N % 4) == 0 && (reinterpret_cast<uintptr_t>(p.scores) & 15) == 0;
+        for (int stage = can_stage ? 1 : 0; stage >= 0; --stage) {
+            const int64_t sb = stage ? tpc * N * 4 : 0;
+            if (sb > kMaxSmem) continue;
+            for (int C = copies_for(N); C >= 1; C >>= 1) {
+                const Layout L = make_layout(kMetroIds, N, 1, r, slice, C, 1, false, static_cast<int>(sb));
+                if (L.total <= kMaxSmem) {
+                    p.slice = slice;
+                    p.staged = 1;
+                    p.C = C;
+                    p.score_bytes = static_cast<int32_t>(sb);
+                    R = r;
+                    return L.total;
+                }
             }
         }
     }
     return METRO_EDIMS;
 }
 
+size_t metro_scores_workspace_bytes(int32_t N) { return N > 0 ? (size_t)N * 8 + 16 : 0; }
+
 int metro_route_scores_v1(const float *scores, int64_t num_tokens, int32_t top_k, const uint32_t *mask, int32_t N,
                           int32_t G, int32_t *topk_ids, int32_t *loads, int32_t *choice, int32_t *rank_counts,
-                          int32_t *lam, int32_t *pair_rank, int32_t *status, int32_t cluster_ctas, void *stream) {
+                          int32_t *lam, int32_t *pair_rank, int32_t *status, void *ws, int32_t cluster_ctas,
+                          void *stream) {
     if ((!scores && num_tokens > 0) || (!topk_ids && num_tokens > 0) || !mask || !choice || !rank_counts ||
         !lam || !status || num_tokens < 0 || top_k < 1)
         return METRO_EARG;
@@ -1553,10 +1689,23 @@ int metro_route_scores_v1(const float *scores, int64_t num_tokens, int32_t top_k
     p.num_pairs = num_tokens * top_k; p.mask = mask; p.N = N; p.G = G;
     p.loads = loads; p.choice = choice; p.rank_counts = rank_counts; p.lam = lam;
     p.pair_rank = pair_rank; p.status = status; p.stamps = g_stamps;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (ws && (cluster_ctas < 0 || (cluster_ctas == 0 && num_tokens > kGateWholeGpuMin))) {
+        // whole-GPU gating, last CTA routes
+        p.gate_ws = ws;
+        const int64_t grid64 = (num_tokens + kGateTokens - 1) / kGateTokens;
+        const int grid = grid64 > 0 ? static_cast<int>(grid64) : 1;
+        if (grid64 > INT32_MAX) return METRO_EDIMS;
+        const int smem = make_layout(kMetroLoads, N, 1, 1, 0, 1, 0).total;
+        cudaError_t e;
+        if (N <= 128) e = launch_plain(metro_gate_kernel<1, 4>, grid, smem, s, p);
+        else if (N <= 256) e = launch_plain(metro_gate_kernel<1, 8>, grid, smem, s, p);
+        else e = launch_plain(metro_gate_kernel<1, 16>, grid, smem, s, p);
+        return e == cudaSuccess ? METRO_OK : cuda_fail(e);
+    }
     int R = 1;
     const int smem = plan_gate(num_tokens, top_k, N, cluster_ctas, p, R);
     if (smem < 0) return smem;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (N <= 128) return launch(metro_ids_kernel<1, false, 4>, R, smem, s, p);
     if (N <= 256) return launch(metro_ids_kernel<1, false, 8>, R, smem, s, p);
     return launch(metro_ids_kernel<1, false, 16>, R, smem, s, p);

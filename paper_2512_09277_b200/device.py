@@ -188,12 +188,17 @@ class Router:
 
     def route_scores(self, scores: torch.Tensor, top_k: int, out: Optional[RouteResult] = None,
                      topk_ids: Optional[torch.Tensor] = None, pair_rank: bool = True,
-                     stream: Optional[torch.cuda.Stream] = None):
+                     stream: Optional[torch.cuda.Stream] = None, whole_gpu: Optional[bool] = None):
         """Gating top-k fused with METRO (metro_route_scores_v1): ``scores`` fp32
         [B, N] router scores of the all-gathered tokens -> (topk_ids int32 [B, k],
         RouteResult).  Each token's ids are its k largest scores, largest first,
         ties to the lower expert id (the reference generator's order,
-        core.py:319-326)."""
+        core.py:319-326).
+
+        ``whole_gpu=True``: every SM takes top-k for 32 tokens and the last CTA
+        routes (a zeroed workspace owned by this Router; use one Router per
+        stream).  ``False``: the routing cluster also takes the top-k.  ``None``
+        (default): the library picks by batch size."""
         if self.kind != "metro":
             raise ValidationError("route_scores is the METRO router's fused gating entry point")
         p = self.placement
@@ -210,10 +215,21 @@ class Router:
         if out is None:
             out = self.alloc(B * k, pair_rank=pair_rank, top_k=k)
         s = _stream(p.device, stream)
+        ws = None
+        cl = self.cluster_ctas
+        if whole_gpu is True:
+            cl = -1
+        elif whole_gpu is None and cl != 0:
+            pass  # an explicit cluster size on the Router selects the cluster variant
+        if whole_gpu is not False:
+            if getattr(self, "_gate_ws", None) is None:
+                nb = _native.lib().metro_scores_workspace_bytes(p.num_experts)
+                self._gate_ws = torch.zeros(nb, dtype=torch.uint8, device=p.device)
+            ws = self._gate_ws.data_ptr()
         rc = _native.lib().metro_route_scores_v1(
             scores.data_ptr(), B, k, p.mask.data_ptr(), p.num_experts, p.num_ranks, topk_ids.data_ptr(),
             _ptr(out.loads), out.choice.data_ptr(), out.rank_counts.data_ptr(), out.lam.data_ptr(),
-            _ptr(out.pair_rank), out.status.data_ptr(), self.cluster_ctas, s)
+            _ptr(out.pair_rank), out.status.data_ptr(), ws, cl, s)
         _native.check_rc(rc, "metro_route_scores_v1")
         return topk_ids, out
 

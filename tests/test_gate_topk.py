@@ -33,11 +33,11 @@ def _cuda():
     torch.cuda.init()
 
 
-def _fused(scores, k, A, cluster=0):
+def _fused(scores, k, A, cluster=0, whole_gpu=None):
     pl = DevicePlacement(A)
     r = Router(pl, "metro", cluster)
     st = torch.from_numpy(np.ascontiguousarray(scores, np.float32)).cuda()
-    ids, out = r.route_scores(st, k)
+    ids, out = r.route_scores(st, k, whole_gpu=whole_gpu)
     out.check()
     return ids.cpu().numpy(), out
 
@@ -54,11 +54,14 @@ def _check_routing(ids, out, A):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("cluster", [0, 1, 2, 4, 8, 16])
+@pytest.mark.parametrize("cluster", ["gpu", 0, 1, 2, 4, 8, 16])
 def test_fused_gate_golden(_cuda, gate, cluster):
     for c in gate:
         A = make_placement(c["N"], c["G"], 1.5, 7).matrix
-        ids, out = _fused(c["scores"], c["k"], A, cluster)
+        if cluster == "gpu":
+            ids, out = _fused(c["scores"], c["k"], A, whole_gpu=True)
+        else:
+            ids, out = _fused(c["scores"], c["k"], A, cluster, whole_gpu=False)
         assert (ids == c["ids"]).all(), (c["N"], c["k"], cluster)
         _check_routing(ids, out, A)
 
@@ -77,7 +80,8 @@ def test_fused_gate_random_with_ties(_cuda):
             sc = rng.integers(-3, 4, size=(B, n)).astype(np.float32)
         else:
             sc = rng.standard_normal((B, n)).astype(np.float32)
-        ids, out = _fused(sc, k, A, int(rng.choice([0, 1, 4, 16])))
+        cl = int(rng.choice([-1, 0, 1, 4, 16]))
+        ids, out = _fused(sc, k, A, max(cl, 0), whole_gpu=True if cl < 0 else (None if cl == 0 else False))
         ref = oracle.gate_topk(sc, k) if B else np.zeros((0, k), np.int32)
         assert (ids == ref).all(), it
         if B:
@@ -88,9 +92,18 @@ def test_fused_gate_random_with_ties(_cuda):
 def test_fused_gate_limits_and_errors(_cuda):
     A = make_placement(256, 8, 1.5, 7).matrix
     sc = np.random.default_rng(1).standard_normal((4096, 256)).astype(np.float32)
-    ids, out = _fused(sc, 8, A)
-    assert (ids == oracle.gate_topk(sc, 8)).all()
-    _check_routing(ids, out, A)
+    for whole in (True, False, None):
+        ids, out = _fused(sc, 8, A, whole_gpu=whole)
+        assert (ids == oracle.gate_topk(sc, 8)).all()
+        _check_routing(ids, out, A)
+    # the workspace is left zeroed: repeated launches on one router agree
+    pl = DevicePlacement(A)
+    r = Router(pl, "metro")
+    st = torch.from_numpy(sc[:1000]).cuda()
+    for _ in range(3):
+        ids, out = r.route_scores(st, 8)
+        out.check()
+        _check_routing(ids.cpu().numpy(), out, A)
     pl = DevicePlacement(A)
     r = Router(pl, "metro")
     with pytest.raises(ValidationError):
