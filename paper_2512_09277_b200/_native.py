@@ -78,6 +78,11 @@ def lib() -> ctypes.CDLL:
         "metro_host_workspace_bytes": ([i64, i32, i32], ctypes.c_size_t),
         "metro_route_host_v1": ([P, i64, P, i32, i32, P, P, P, i32, i32, P], ctypes.c_int),
         "metro_debug_set_stamps": ([P], None),
+        "metro_server_create_v1": ([P, i32, i32, i64, i32, P], ctypes.c_int),
+        "metro_server_route_v1": ([P, P, i64, P, P], ctypes.c_int),
+        "metro_server_launches": ([P], ctypes.c_int64),
+        "metro_server_destroy_v1": ([P], ctypes.c_int),
+        "metro_server_debug_stamps": ([P, P], ctypes.c_int),
         "metro_replica_table": ([P, i32, i32, P, P], ctypes.c_int),
         "metro_dispatch_layout_v1": ([P, P, i64, P, P, i32, i32, i32, P, P, P, i32, P], ctypes.c_int),
     }
@@ -91,7 +96,7 @@ def lib() -> ctypes.CDLL:
     return L
 
 
-HEADERS = ("metro_route.h", "moe_gemm.h", "dispatch_layout.h")
+HEADERS = ("metro_route.h", "metro_serve.h", "moe_gemm.h", "dispatch_layout.h")
 
 
 def exported_symbols() -> list:

@@ -311,3 +311,86 @@ class HostRouter:
         )
         _native.check_rc(rc, "metro_route_host_v1")
         return self._out_np
+
+
+class ServedRouter:
+    """End-to-end METRO for host callers through a persistent router
+    (include/metro_serve.h): one resident CTA waits on a doorbell in pinned host
+    memory, so a call costs two PCIe round trips plus the routing itself instead
+    of a kernel launch + stream synchronise (``HostRouter``).
+
+    Same buffers and result layout as ``HostRouter``: write the batch into
+    ``ids`` and call ``run(num_pairs)``; results land in ``out`` ([status 4 |
+    lam | pad 3 | rank_counts G | choice N]) and ``pair_rank``.  The resident
+    CTA occupies one SM and exits by itself after ``idle_timeout_us`` without a
+    request (the next call relaunches it), so a device-wide synchronise
+    elsewhere waits at most that long.  ``close()`` (or the context manager)
+    stops it.  One ServedRouter per placement; not thread-safe (one caller at a
+    time).
+    """
+
+    def __init__(self, placement: DevicePlacement, max_pairs: int, idle_timeout_us: int = 200_000):
+        self.placement = placement
+        self.max_pairs = int(max_pairs)
+        L = _native.lib()
+        n, g = placement.num_experts, placement.num_ranks
+        self.ids = torch.zeros(max(self.max_pairs, 4), dtype=torch.int32).pin_memory()
+        self.out = torch.zeros(8 + g + n, dtype=torch.int32).pin_memory()
+        self.pair_rank = torch.zeros(max(self.max_pairs, 4), dtype=torch.int32).pin_memory()
+        self._out_np = self.out.numpy()
+        h = ctypes.c_void_p()
+        with torch.cuda.device(placement.device):
+            rc = L.metro_server_create_v1(placement.mask.data_ptr(), n, g, self.max_pairs, int(idle_timeout_us),
+                                          ctypes.byref(h))
+        _native.check_rc(rc, "metro_server_create_v1")
+        self._h = h
+        self._fn = L.metro_server_route_v1
+        self._args = [h, ctypes.c_void_p(self.ids.data_ptr()), ctypes.c_int64(0),
+                      ctypes.c_void_p(self.out.data_ptr()), ctypes.c_void_p(self.pair_rank.data_ptr())]
+
+    def run(self, num_pairs: int) -> np.ndarray:
+        """Route ids[:num_pairs] (already written into self.ids); synchronous."""
+        if self._h is None:
+            raise ValidationError("ServedRouter is closed")
+        if not 0 <= num_pairs <= self.max_pairs:
+            raise ValidationError("batch larger than the ServedRouter capacity")
+        self._args[2].value = num_pairs
+        rc = self._fn(*self._args)
+        if rc:
+            _native.check_rc(rc, "metro_server_route_v1")
+        return self._out_np
+
+    def route(self, topk_ids) -> np.ndarray:
+        """Copy a host batch (numpy / CPU tensor, [B, k] int) into the pinned
+        buffer and route it; returns ``out`` (raises on a data error, like the
+        reference's ValidationError / AssertionError)."""
+        a = np.ascontiguousarray(np.asarray(topk_ids, dtype=np.int32)).reshape(-1)
+        if a.size > self.max_pairs:
+            raise ValidationError("batch larger than the ServedRouter capacity")
+        self.ids.numpy()[: a.size] = a
+        out = self.run(a.size)
+        raise_status(out[:4], topk_ids.shape[-1] if getattr(topk_ids, "ndim", 1) >= 2 else 1)
+        return out
+
+    @property
+    def launches(self) -> int:
+        """Launches of the resident CTA (1 + relaunches after idle exits)."""
+        return int(_native.lib().metro_server_launches(self._h)) if self._h is not None else 0
+
+    def close(self) -> None:
+        if self._h is not None:
+            rc = _native.lib().metro_server_destroy_v1(self._h)
+            self._h = None
+            _native.check_rc(rc, "metro_server_destroy_v1")
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -10,7 +10,7 @@ import time
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2512_09277_b200 import DevicePlacement, HostRouter, Router, _native  # noqa: E402
+from paper_2512_09277_b200 import DevicePlacement, HostRouter, Router, ServedRouter, _native  # noqa: E402
 from paper_2512_09277_b200.placement import gen_zipf_topk, make_placement  # noqa: E402
 
 
@@ -48,6 +48,10 @@ def main():
             torch.cuda.synchronize()
             dts.append(e0.elapsed_time(e1) * 1e3)
         res[f"device_{'zc' if zc else 'copy'}_us"] = statistics.median(dts)
+    with ServedRouter(pl, 8192) as sr:
+        sr.ids.numpy()[:] = ids.numpy()
+        res["served_us"] = tmed(lambda: sr.run(8192), n=20000)
+        res["served_launches"] = sr.launches
     r = Router(pl, "metro")
     d_ids = ids.to(dev)
     out = r.alloc(8192, top_k=8)

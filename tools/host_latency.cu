@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cuda_runtime.h>
 #include "../include/metro_route.h"
+#include "../include/metro_serve.h"
 
 __global__ void empty_kernel() {}
 
@@ -58,6 +59,38 @@ int main() {
             metro_route_v1(dids, P, dmask, N, G, nullptr, dout + 8 + G, dout + 8, dout + 4, dout + 8 + G + N, dout, R, s);
             cudaStreamSynchronize(s);
         });
+    }
+    // persistent server (metro_serve.h): both fence variants
+    struct Var { const char *name, *fence, *stagger; };
+    const Var vars[] = {
+        {"served release/st500", "release", "500"}, {"served release/st250", "release", "250"},
+        {"served release/st1000", "release", "1000"}, {"served one/st500", "one", "500"},
+        {"served all/st500", "all", "500"},
+    };
+    for (const Var &v : vars) {
+        setenv("METRO_SERVE_FENCE", v.fence, 1);
+        setenv("METRO_SERVE_STAGGER_NS", v.stagger, 1);
+        for (int np : {P, 0}) {
+            metro_server *srv = nullptr;
+            int rc = metro_server_create_v1(dmask, N, G, P, 500000, &srv);
+            if (rc) { printf("create rc %d\n", rc); exit(1); }
+            char name[96]; snprintf(name, sizeof name, "%s%s", v.name, np ? "" : " (empty batch)");
+            double acc[8] = {0};
+            int nacc = 0;
+            bench(name, [&] {
+                int rc2 = metro_server_route_v1(srv, ids, np, out, pr);
+                if (rc2) { printf("route rc %d\n", rc2); exit(1); }
+                int64_t st[8];
+                metro_server_debug_stamps(srv, st);
+                for (int i = 1; i < 8; ++i) acc[i] += st[i];
+                ++nacc;
+            });
+            printf("  phases (mean ns): staged %.0f routed %.0f stored %.0f fence %.0f | total %.0f ns, %.0f MHz | "
+                   "doorbell RTT %.0f ns | status %d lam %d launches %lld\n",
+                   acc[1] / nacc, acc[2] / nacc, acc[3] / nacc, acc[4] / nacc, acc[6] / nacc,
+                   acc[5] / acc[6] * 1e3, acc[7] / nacc, out[0], out[4], (long long)metro_server_launches(srv));
+            metro_server_destroy_v1(srv);
+        }
     }
     printf("status %d lam %d\n", out[0], out[4]);
     return 0;

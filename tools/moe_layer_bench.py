@@ -118,7 +118,7 @@ def run(batches=4, reps=5, B=1024, ratio=1.5, seed0=1000):
                 lambda st: lay(ids, pr, out=lout, stream=st), reps, inner=200)
             del pipe
         rows.append(res)
-        print(json.dumps(res), flush=True)
+        print(json.dumps(res), file=sys.stderr, flush=True)
     summ = {}
     for kind in ("metro", "eplb"):
         summ[kind] = {key: statistics.mean(r[kind][key] for r in rows)
