@@ -256,7 +256,7 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
     import torch.distributed as dist
 
     from paper_2512_09277_b200 import DevicePlacement, HostRouter, Router
-    from paper_2512_09277_b200.dist import DistributedRouter, allgather_topk
+    from paper_2512_09277_b200.dist import DistributedRouter, FusedAllGatherRouter, allgather_topk
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
@@ -378,6 +378,41 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
             K_eff = K
             method = {"method": "per step: 256 MiB L2 flush + all-gather + route; flush-only loop "
                                 "subtracted; one event pair per K-step loop; max over ranks"}
+            # the product path: exchange + route fused in ONE kernel per rank over NVLink
+            # peer memory (metro_exchange.h); the NCCL all-gather + route above is the
+            # baseline it replaces.  Any rank failing to set it up or to complete the
+            # warm-up exchange disables it on every rank (no hang, no partial run).
+            fused_ms, fused_err = None, None
+            fz = None
+            try:
+                fz = FusedAllGatherRouter(pl, lt, k)
+                for i in range(3):
+                    fz.step(local_pool[i % POOL])
+                torch.cuda.synchronize()
+                st = int(fz.out.status[0].item())
+                if st != 0:
+                    raise RuntimeError(f"fused exchange status {st}")
+                ag_route(2)  # same batch through the NCCL path: identical routing required
+                torch.cuda.synchronize()
+                if not (torch.equal(fz.out.choice, out.choice) and int(fz.out.lam.item()) == int(out.lam.item())):
+                    raise RuntimeError("fused routing differs from the NCCL path")
+                bad = 0
+            except Exception as ex:  # noqa: BLE001 -- reported in the JSON line
+                fused_err, bad = repr(ex)[:200], 1
+            flag = torch.tensor([bad], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+            if int(flag.item()) == 0:
+                tfz = loop_ms(K, lambda i: fz.step(local_pool[i % POOL]), True)
+                fused_ms = max_over_ranks([(tfz - tf) / K])[0]
+                nccl_ms = step_ms
+                step_ms = fused_ms
+                method["method"] = ("per step: 256 MiB L2 flush + fused exchange+route kernel (metro_exchange.h, "
+                                    "NVLink peer stores); flush-only loop subtracted; one event pair per K-step "
+                                    "loop; max over ranks")
+                method["nccl_allgather_plus_route_us"] = nccl_ms * 1e3
+            else:
+                method["fused_unavailable"] = fused_err or "another rank failed"
+            method["fused_exchange_route_us"] = None if fused_ms is None else fused_ms * 1e3
         sync_all()
 
     # lambda METRO vs EPLB over the exact Zipf batches (device outputs)
@@ -492,6 +527,7 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
     if world > 1:
         recv = (world - 1) * lt * k * 4
         res["nvlink"] = {"allgather_recv_bytes_per_rank": recv,
+                         "fused_exchange_recv_bytes_per_rank": (world - 1) * (cfg["N"] + 3) * 8,
                          "achieved_gbs": recv / (ag_ms * 1e-3) / 1e9, "peak_gbs": 770.0,
                          "frac": recv / (ag_ms * 1e-3) / 1e9 / 770.0,
                          "peak_source": "measured peer copy, B200_PROFILING.md"}
@@ -535,6 +571,8 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
 
 def main():
     args = parse_args()
+    # a peer that never joins the fused exchange is reported after 2 s, never a hang
+    os.environ.setdefault("METRO_PEER_TIMEOUT_MS", "2000")
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

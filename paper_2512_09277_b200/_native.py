@@ -13,7 +13,8 @@ from typing import Optional
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(_HERE, "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "libmetro_b200.so")
+# METRO_B200_LIB: load another build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("METRO_B200_LIB") or os.path.join(LIB_DIR, "libmetro_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 ABI_VERSION = 1
@@ -24,6 +25,7 @@ ERR_ID_RANGE = 1
 ERR_NO_REPLICA = 2
 ERR_LOAD_RANGE = 3
 ERR_PAIR_RANK = 4
+ERR_PEER_TIMEOUT = 5
 EARG = -1
 EDIMS = -2
 ECUDA = -3
@@ -83,6 +85,15 @@ def lib() -> ctypes.CDLL:
         "metro_server_launches": ([P], ctypes.c_int64),
         "metro_server_destroy_v1": ([P], ctypes.c_int),
         "metro_server_debug_stamps": ([P, P], ctypes.c_int),
+        "metro_exchange_bytes": ([i32, i32, i64], ctypes.c_size_t),
+        "metro_allgather_route_v1": ([P, i64, i32, i32, P, i64, P, i32, i32, P, P, P, P, P, P, P, P],
+                                     ctypes.c_int),
+        "metro_allgather_debug_stamps": ([P], None),
+        "metro_exchange_alloc": ([ctypes.c_size_t, P], ctypes.c_int),
+        "metro_exchange_free": ([P], ctypes.c_int),
+        "metro_ipc_get_handle": ([P, P], ctypes.c_int),
+        "metro_ipc_open_handle": ([P, P], ctypes.c_int),
+        "metro_ipc_close_handle": ([P], ctypes.c_int),
         "metro_replica_table": ([P, i32, i32, P, P], ctypes.c_int),
         "metro_dispatch_layout_v1": ([P, P, i64, P, P, i32, i32, i32, P, P, P, i32, P], ctypes.c_int),
     }
@@ -96,7 +107,7 @@ def lib() -> ctypes.CDLL:
     return L
 
 
-HEADERS = ("metro_route.h", "metro_serve.h", "moe_gemm.h", "dispatch_layout.h")
+HEADERS = ("metro_route.h", "metro_serve.h", "metro_exchange.h", "moe_gemm.h", "dispatch_layout.h")
 
 
 def exported_symbols() -> list:

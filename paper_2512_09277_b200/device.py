@@ -121,6 +121,8 @@ def raise_status(status: np.ndarray, top_k: int = 1) -> None:
         raise AssertionError("placement invariant: every expert has a replica")
     if code == _native.ERR_LOAD_RANGE:
         raise ValidationError("load does not fit the device loads path")
+    if code == _native.ERR_PEER_TIMEOUT:
+        raise _native.NativeLibraryError(f"peer rank {int(status[1])} did not join the exchange (timeout)")
     if code == _native.ERR_PAIR_RANK:
         pair = int(np.uint32(status[1])) | (int(np.uint32(status[2])) << 32)
         raise ValidationError(f"token {pair // max(top_k, 1)}: rank {int(status[3])} hosts no replica of its expert")

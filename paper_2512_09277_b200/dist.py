@@ -126,3 +126,150 @@ class DistributedRouter:
     def own_pair_rank(self) -> torch.Tensor:
         """EP rank serving each (token, slot) of this rank's own tokens."""
         return self.out.pair_rank[local_slice(self.rank, self.local_tokens, self.top_k)]
+
+
+class ExchangeRoute:
+    """One EP rank's fused all-gather + METRO launch (include/metro_exchange.h).
+
+    The rank's exchange buffer and the device-visible addresses of every rank's
+    buffer are given (``peer_ptrs[rank]`` is the own one).  Use
+    ``FusedAllGatherRouter`` (one process per GPU, CUDA IPC over the process
+    group) or ``virtual_ranks`` (all ranks in one process on one device, for
+    tests and single-GPU measurement) to build them.
+    """
+
+    def __init__(self, placement: DevicePlacement, rank: int, world: int, local_tokens: int, top_k: int,
+                 peer_ptrs, max_local_pairs: int, gather_ids: bool = False):
+        import ctypes
+
+        from . import _native
+
+        if not 1 <= world <= 32 or not 0 <= rank < world:
+            raise ValueError(f"rank {rank} / world {world} outside 1..32")
+        self.placement, self.rank, self.world = placement, rank, world
+        self.local_tokens, self.top_k = local_tokens, top_k
+        self.local_pairs = local_tokens * top_k
+        self.max_local_pairs = max_local_pairs
+        dev = placement.device
+        i32 = dict(dtype=torch.int32, device=dev)
+        n, g = placement.num_experts, placement.num_ranks
+        self.local = torch.zeros((local_tokens, top_k), **i32)
+        self.out = RouteResult(kind="metro", loads=torch.empty(n, **i32), choice=torch.empty(n, **i32), x=None,
+                               rank_counts=torch.empty(g, **i32), lam=torch.empty(1, **i32),
+                               pair_rank=torch.empty(self.local_pairs, **i32), status=torch.zeros(4, **i32),
+                               top_k=top_k)
+        self.gathered = torch.zeros((world * local_tokens, top_k), **i32) if gather_ids else None
+        self._peers = (ctypes.c_void_p * world)(*[int(p) for p in peer_ptrs])
+        self._fn = _native.lib().metro_allgather_route_v1
+
+    def step(self, local_ids: Optional[torch.Tensor] = None,
+             stream: Optional[torch.cuda.Stream] = None) -> RouteResult:
+        """One layer: exchange + route (stream-ordered, graph-capturable).  Every
+        rank must call it the same number of times, in the same order."""
+        from . import _native
+
+        ids = self.local if local_ids is None else local_ids
+        if ids.numel() != self.local_pairs or ids.dtype != torch.int32 or not ids.is_cuda:
+            raise ValueError("local_ids must be int32 CUDA [local_tokens, top_k]")
+        ids = ids.contiguous()
+        p = self.placement
+        s = (stream if stream is not None else torch.cuda.current_stream(p.device)).cuda_stream
+        o = self.out
+        rc = self._fn(ids.data_ptr(), self.local_pairs, self.rank, self.world, self._peers, self.max_local_pairs,
+                      p.mask.data_ptr(), p.num_experts, p.num_ranks, o.loads.data_ptr(), o.choice.data_ptr(),
+                      o.rank_counts.data_ptr(), o.lam.data_ptr(), o.pair_rank.data_ptr(),
+                      None if self.gathered is None else self.gathered.data_ptr(), o.status.data_ptr(), s)
+        _native.check_rc(rc, "metro_allgather_route_v1")
+        return o
+
+
+class _ExchangeBuffer:
+    """A zeroed exchange buffer from metro_exchange_alloc (freed on close)."""
+
+    def __init__(self, nbytes: int, device: torch.device):
+        import ctypes
+
+        from . import _native
+
+        self.ptr = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            _native.check_rc(_native.lib().metro_exchange_alloc(nbytes, ctypes.byref(self.ptr)),
+                             "metro_exchange_alloc")
+        self.device = device
+
+    def close(self):
+        from . import _native
+
+        if self.ptr:
+            with torch.cuda.device(self.device):
+                _native.lib().metro_exchange_free(self.ptr)
+            self.ptr = None
+
+
+def exchange_bytes(placement: DevicePlacement, world: int, max_local_pairs: int) -> int:
+    from . import _native
+
+    return int(_native.lib().metro_exchange_bytes(placement.num_experts, world, max_local_pairs))
+
+
+def virtual_ranks(placement: DevicePlacement, world: int, local_tokens: int, top_k: int,
+                  gather_ids: bool = False):
+    """``world`` EP ranks in ONE process on ONE device, each with its own exchange
+    buffer, addressing the others' buffers directly: the same kernel and protocol
+    as across GPUs (peer addresses are plain device addresses here).  Launch the
+    ranks' steps on distinct streams -- they wait for each other.  Returns
+    (routers, buffers); close the buffers when done."""
+    max_local = -(-local_tokens * top_k // 4) * 4
+    nbytes = exchange_bytes(placement, world, max_local)
+    bufs = [_ExchangeBuffer(nbytes, placement.device) for _ in range(world)]
+    ptrs = [b.ptr.value for b in bufs]
+    routers = [ExchangeRoute(placement, r, world, local_tokens, top_k, ptrs, max_local, gather_ids)
+               for r in range(world)]
+    return routers, bufs
+
+
+class FusedAllGatherRouter(ExchangeRoute):
+    """Fused all-gather + METRO over NVLink peer memory, one process per GPU.
+
+    The exchange buffers are allocated per rank and mapped into every peer with
+    CUDA IPC handles all-gathered over ``group`` (``torch.distributed`` is the
+    plumbing; the exchange itself is the kernel's P2P stores).  Replaces
+    ``DistributedRouter``'s NCCL all-gather + route with one launch.
+    """
+
+    def __init__(self, placement: DevicePlacement, local_tokens: int, top_k: int, group=None,
+                 gather_ids: bool = False):
+        import ctypes
+
+        from . import _native
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        max_local = -(-local_tokens * top_k // 4) * 4
+        self._buf = _ExchangeBuffer(exchange_bytes(placement, world, max_local), placement.device)
+        L = _native.lib()
+        h = ctypes.create_string_buffer(64)
+        _native.check_rc(L.metro_ipc_get_handle(self._buf.ptr, h), "metro_ipc_get_handle")
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(h.raw), group=group)
+        self._opened = []
+        ptrs = []
+        with torch.cuda.device(placement.device):
+            for q in range(world):
+                if q == rank:
+                    ptrs.append(self._buf.ptr.value)
+                    continue
+                p = ctypes.c_void_p()
+                _native.check_rc(L.metro_ipc_open_handle(ctypes.create_string_buffer(handles[q], 64),
+                                                         ctypes.byref(p)), "metro_ipc_open_handle")
+                self._opened.append(p)
+                ptrs.append(p.value)
+        super().__init__(placement, rank, world, local_tokens, top_k, ptrs, max_local, gather_ids)
+        dist.barrier(group=group)
+
+    def close(self):
+        from . import _native
+
+        for p in self._opened:
+            _native.lib().metro_ipc_close_handle(p)
+        self._opened = []
+        self._buf.close()
