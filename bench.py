@@ -357,7 +357,31 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
             kern_ms = step_ms
             ag_ms = 0.0
             method = {"method": "graph-replayed back-to-back over a {:.0f} MiB pool of {} distinct batches (> L2)"
-                      .format(P * per_batch / 2 ** 20, P)}
+                      .format(P * per_batch / 2 ** 20, P),
+                      "pdl": "programmatic dependent launch: each routing kernel's shared-memory prologue "
+                             "overlaps the previous kernel; it waits for that kernel's completion before "
+                             "reading its ids (as behind the gating kernel in a decode step)"}
+            del graphs
+            # the same pool measurement with PDL off (every launch fully serialised)
+            from paper_2512_09277_b200 import _native
+
+            _native.lib().metro_set_pdl(0)
+            graphs = []
+            for c0 in range(0, P, chunk):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    for j in range(c0, min(P, c0 + chunk)):
+                        router.route(big[j], out=out)
+                graphs.append(g)
+            _native.lib().metro_set_pdl(1)
+            graphs[0].replay()
+            torch.cuda.synchronize()
+            e0.record()
+            for g in graphs:
+                g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            method["no_pdl_us"] = e0.elapsed_time(e1) / P * 1e3
             del graphs, big
             # (b) context: eager launch after a 256 MiB L2 flush, flush time subtracted
             Kb = min(K, 2000)

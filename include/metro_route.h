@@ -183,6 +183,14 @@ METRO_API int metro_route_host_v1(const int32_t *topk_ids_host, int64_t num_pair
                                   void *dev_workspace, int32_t *host_out, int32_t *pair_rank_host,
                                   int32_t cluster_ctas, int32_t flags, void *stream);
 
+/* Programmatic dependent launch of the routing kernels (default on; METRO_PDL=0
+ * in the environment or metro_set_pdl(0) turns it off).  With it a routing
+ * kernel launched behind another kernel in the stream (the gating kernel in a
+ * decode step) runs its shared-memory prologue while that kernel finishes and
+ * waits (griddepcontrol.wait) for its completion before the first global
+ * access; it also lets the next kernel do the same. */
+METRO_API void metro_set_pdl(int32_t enable);
+
 /* Debug / tuning: per-phase clock64 stamps of CTA 0 of the next metro_route_v1
  * launch in this process are written to `stamps` (device, >= 16 int64) when set;
  * pass NULL to disable.  Not for production use. */

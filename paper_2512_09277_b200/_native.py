@@ -80,6 +80,7 @@ def lib() -> ctypes.CDLL:
         "metro_host_workspace_bytes": ([i64, i32, i32], ctypes.c_size_t),
         "metro_route_host_v1": ([P, i64, P, i32, i32, P, P, P, i32, i32, P], ctypes.c_int),
         "metro_debug_set_stamps": ([P], None),
+        "metro_set_pdl": ([i32], None),
         "metro_server_create_v1": ([P, i32, i32, i64, i32, P], ctypes.c_int),
         "metro_server_route_v1": ([P, P, i64, P, P], ctypes.c_int),
         "metro_server_launches": ([P], ctypes.c_int64),

@@ -52,12 +52,16 @@ __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) 
     const int n_local = rem_pairs <= 0 ? 0 : static_cast<int>(rem_pairs < p.slice ? rem_pairs : p.slice);
     constexpr bool GATE = GATE_NPL > 0;
     const StagePlan sp = stage_plan<W>(p, beg, n_local, !GATE && p.staged != 0);
-    if (threadIdx.x == 0) stage_issue(p, L, smem, beg, sp);
-    if (R > 1) cluster_arrive_release();  // after thread 0 initialised the mbarriers
-    stamp(p, 0);
+    // PDL: shared-memory prologue while the previous kernel in the stream finishes;
+    // no global access before griddep_wait (the ids are that kernel's output)
+    griddep_launch_dependents();
     int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
     init_misc(misc);
     zero_smem(smem, L.aux, L.part);  // forced counts + histogram
+    griddep_wait();
+    if (threadIdx.x == 0) stage_issue(p, L, smem, beg, sp);
+    if (R > 1) cluster_arrive_release();  // after thread 0 initialised the mbarriers
+    stamp(p, 0);
     stage_rest(p, L, smem, beg, n_local, !GATE && p.staged != 0, sp);
     __syncthreads();
     if (GATE) {
@@ -150,6 +154,8 @@ __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) 
 // workspace for the next launch.
 template <int W, int NPL>
 __global__ void __launch_bounds__(kThreads, 1) metro_gate_kernel(const Params p) {
+    griddep_launch_dependents();
+    griddep_wait();  // PDL launch: no global access before the previous kernel completes
     extern __shared__ __align__(128) unsigned char smem[];
     const Layout L = make_layout(kMetroLoads, p.N, W, 1, 0, 1, 0);
     const int tid = threadIdx.x, N = p.N, k = p.top_k;
@@ -231,6 +237,8 @@ __global__ void __launch_bounds__(kThreads, 1) metro_gate_kernel(const Params p)
 // METRO from loads (compat route_metro(T, A)) or from a caller order (metro-parallel).
 template <int W>
 __global__ void __launch_bounds__(kThreads, 1) metro_loads_kernel(const Params p, int ordered) {
+    griddep_launch_dependents();
+    griddep_wait();  // PDL launch: no global access before the previous kernel completes
     extern __shared__ __align__(128) unsigned char smem[];
     const Layout L = make_layout(ordered ? kMetroOrdered : kMetroLoads, p.N, W, 1, 0, 1, 0);
     const StagePlan sp = stage_plan<W>(p, 0, 0, false);
@@ -350,6 +358,8 @@ __device__ bool eplb_counts_and_x(const Params &p, const Layout &L, unsigned cha
 
 template <int W, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) eplb_ids_kernel(const Params p) {
+    griddep_launch_dependents();
+    griddep_wait();  // PDL launch: no global access before the previous kernel completes
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t R = cluster_nctarank(), rank = cluster_ctarank();
     const Layout L = make_layout(kEplbIds, p.N, W, R, p.slice, p.C, p.staged, PAIR);
@@ -437,6 +447,8 @@ __global__ void __launch_bounds__(kThreads, 1) eplb_ids_kernel(const Params p) {
 
 template <int W>
 __global__ void __launch_bounds__(kThreads, 1) eplb_loads_kernel(const Params p) {
+    griddep_launch_dependents();
+    griddep_wait();  // PDL launch: no global access before the previous kernel completes
     extern __shared__ __align__(128) unsigned char smem[];
     const Layout L = make_layout(kEplbLoads, p.N, W, 1, 0, 1, 0);
     const StagePlan sp = stage_plan<W>(p, 0, 0, false);
@@ -487,6 +499,15 @@ static cudaError_t prepare(K kernel) {
     return err;
 }
 
+static int g_pdl = -1;  // -1: from METRO_PDL (default on); 0 / 1: metro_set_pdl
+static bool pdl_enabled() {
+    if (g_pdl < 0) {
+        const char *v = getenv("METRO_PDL");
+        g_pdl = (v && strcmp(v, "0") == 0) ? 0 : 1;
+    }
+    return g_pdl != 0;
+}
+
 template <typename K, typename... Args>
 static int launch(K kernel, int R, int smem, cudaStream_t s, Args... args) {
     cudaError_t e = prepare(kernel);
@@ -496,13 +517,17 @@ static int launch(K kernel, int R, int smem, cudaStream_t s, Args... args) {
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = R;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    // programmatic dependent launch: every kernel launched here calls griddep_wait
+    // before its first global access (METRO_PDL=0 disables, for A/B timing)
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     e = cudaLaunchKernelEx(&cfg, kernel, args...);
     if (e != cudaSuccess) return cuda_fail(e);
     return METRO_OK;
@@ -610,6 +635,7 @@ const char *metro_strerror(int code) {
 int metro_last_cuda_error(void) { return g_last_cuda_error; }
 int metro_mask_words(int32_t G) { return words_for(G); }
 void metro_debug_set_stamps(int64_t *stamps) { g_stamps = stamps; }
+void metro_set_pdl(int32_t enable) { g_pdl = enable ? 1 : 0; }
 
 int metro_pack_placement(const int8_t *A, int32_t N, int32_t G, uint32_t *mask) {
     if (!A || !mask || N < 0 || G < 0) return METRO_EARG;

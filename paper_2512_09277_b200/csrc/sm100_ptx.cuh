@@ -80,6 +80,15 @@ __device__ __forceinline__ void st_async_v4(const void *local, uint32_t cta, uin
                  : "memory");
 }
 
+// Programmatic dependent launch (PDL): let the next kernel in the stream (launched
+// with programmatic stream serialization) start its prologue now; and wait until
+// every prerequisite grid has completed and its memory is visible -- call before
+// the first global-memory access.
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
