@@ -31,14 +31,26 @@ namespace moe {
 
 constexpr int BM = 128;        // weight rows per tile (UMMA M)
 constexpr int BK = 64;         // bf16 elements per 128-byte swizzled row
-constexpr int MAXN = 256;      // tokens per item (UMMA N <= 256)
-constexpr int STAGES = 4;
+constexpr int MAXN = 256;      // tokens per item, wide variant (UMMA N <= 256)
+constexpr int kItemTokens = 64;  // the item chunk of moe_layout_items / build_items
 constexpr int kThreads = 192;  // 4 epilogue warps + TMA warp + MMA warp
 constexpr int A_BYTES = BM * BK * 2;    // 16 KB
-constexpr int B_BYTES = MAXN * BK * 2;  // 32 KB
 constexpr int NMAPS = 5;                // X maps with box heights 16, 32, 64, 128, 256
-constexpr int kSmem = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
-constexpr int TMEM_COLS = 512;          // 2 accumulators x 256 fp32 columns
+// Two tilings of the same kernel.  Decode items carry few tokens, so the narrow
+// variant spends the shared memory on pipeline depth instead of token rows:
+// 8 stages of (16 KB weights + 8 KB tokens) keep 128 KB of weights in flight per
+// SM (the HBM latency x per-SM bandwidth product under load), where the wide one
+// keeps 64 KB.  Both use 197,888 bytes of shared memory.
+template <int NT, int ST>
+struct Tile {
+    static constexpr int kN = NT;                      // tokens per item (UMMA N)
+    static constexpr int kStages = ST;
+    static constexpr int kBBytes = NT * BK * 2;
+    static constexpr int kSmem = 1024 + ST * (A_BYTES + kBBytes) + 256;
+    static constexpr int kTmemCols = 2 * NT < 32 ? 32 : 2 * NT;  // 2 accumulators x NT fp32 columns
+};
+using WideTile = Tile<256, 4>;
+using NarrowTile = Tile<kItemTokens, 8>;
 
 struct Item {
     int e, m_blk, t0, n;
@@ -136,7 +148,9 @@ __device__ __forceinline__ int map_index(int n) {  // smallest box height >= n
     return i;
 }
 
+template <typename TL>
 __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_constant__ Maps maps, const Params p) {
+    constexpr int STAGES = TL::kStages, B_BYTES = TL::kBBytes, MAXN_T = TL::kN, TMEM_COLS = TL::kTmemCols;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char *sA = smem;
@@ -208,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
                 tc_fence_after();
                 const int nmma = (item.n + 15) & ~15;
                 const uint32_t idesc = idesc_bf16(nmma);
-                const uint32_t dcol = tmem_base + static_cast<uint32_t>(acc * MAXN);
+                const uint32_t dcol = tmem_base + static_cast<uint32_t>(acc * MAXN_T);
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
@@ -236,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             mbar_wait(&tfull[acc], aphase);
             tc_fence_after();
             const int row = item.m_blk * BM + warp * 32 + lane;
-            const uint32_t tbase = tmem_base + static_cast<uint32_t>(acc * MAXN) + (static_cast<uint32_t>(warp * 32) << 16);
+            const uint32_t tbase = tmem_base + static_cast<uint32_t>(acc * MAXN_T) + (static_cast<uint32_t>(warp * 32) << 16);
             for (int c = 0; c < item.n; c += 32) {
                 uint32_t v[32];
                 TMEM_LD_X32(tbase + static_cast<uint32_t>(c), v);
@@ -293,7 +307,7 @@ __global__ void __launch_bounds__(kItThreads) layout_items_kernel(const int32_t 
     for (int s0 = 0; s0 < S; s0 += kItThreads) {
         const int s = s0 + tid;
         const int n = (s < S) ? rep_off[b0 + s + 1] - rep_off[b0 + s] : 0;
-        const int c = (n + MAXN - 1) / MAXN;
+        const int c = (n + kItemTokens - 1) / kItemTokens;
         int x = c;  // inclusive scan of chunk counts
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -318,12 +332,12 @@ __global__ void __launch_bounds__(kItThreads) layout_items_kernel(const int32_t 
             for (int mb = 0; mb < mb1; ++mb)
                 for (int j = 0; j < c; ++j) {
                     const int idx = before * mb1 + mb * c + j;
-                    if (idx < cap1) items1[idx] = Item{s, mb, t0 + j * MAXN, min(MAXN, n - j * MAXN)};
+                    if (idx < cap1) items1[idx] = Item{s, mb, t0 + j * kItemTokens, min(kItemTokens, n - j * kItemTokens)};
                 }
             for (int mb = 0; mb < mb2; ++mb)
                 for (int j = 0; j < c; ++j) {
                     const int idx = before * mb2 + mb * c + j;
-                    if (idx < cap2) items2[idx] = Item{s, mb, t0 + j * MAXN, min(MAXN, n - j * MAXN)};
+                    if (idx < cap2) items2[idx] = Item{s, mb, t0 + j * kItemTokens, min(kItemTokens, n - j * kItemTokens)};
                 }
         }
         run += s_w[kItThreads / 32 - 1];
@@ -387,8 +401,8 @@ using namespace moe;
 extern "C" {
 
 static int launch_gemm(const void *W, int32_t E, int32_t M, int32_t K, const void *X, int32_t T,
-                       const int32_t *items, int32_t n_items, const int32_t *n_items_dev, void *Y, int32_t num_ctas,
-                       void *stream) {
+                       const int32_t *items, int32_t n_items, const int32_t *n_items_dev, int32_t max_item_tokens,
+                       void *Y, int32_t num_ctas, void *stream) {
     Maps maps;
     const cuuint64_t wdims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(E)};
     const cuuint64_t wstr[2] = {static_cast<cuuint64_t>(K) * 2, static_cast<cuuint64_t>(M) * K * 2};
@@ -403,7 +417,11 @@ static int launch_gemm(const void *W, int32_t E, int32_t M, int32_t K, const voi
     static std::once_flag attr;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(attr, [] {
-        attr_err = cudaFuncSetAttribute(moe_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        attr_err = cudaFuncSetAttribute(moe_gemm_kernel<WideTile>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        WideTile::kSmem);
+        if (attr_err == cudaSuccess)
+            attr_err = cudaFuncSetAttribute(moe_gemm_kernel<NarrowTile>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            NarrowTile::kSmem);
     });
     if (attr_err != cudaSuccess) {
         g_err = attr_err;
@@ -420,7 +438,11 @@ static int launch_gemm(const void *W, int32_t E, int32_t M, int32_t K, const voi
     prm.K = K;
     prm.Y = static_cast<__nv_bfloat16 *>(Y);
     prm.ldy = M;
-    moe_gemm_kernel<<<grid, kThreads, kSmem, static_cast<cudaStream_t>(stream)>>>(maps, prm);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (max_item_tokens <= NarrowTile::kN)
+        moe_gemm_kernel<NarrowTile><<<grid, kThreads, NarrowTile::kSmem, s>>>(maps, prm);
+    else
+        moe_gemm_kernel<WideTile><<<grid, kThreads, WideTile::kSmem, s>>>(maps, prm);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         g_err = e;
@@ -429,22 +451,39 @@ static int launch_gemm(const void *W, int32_t E, int32_t M, int32_t K, const voi
     return METRO_OK;
 }
 
-METRO_API int moe_grouped_gemm_v1(const void *W, int32_t E, int32_t M, int32_t K, const void *X, int32_t T,
-                        const int32_t *items, int32_t n_items, void *Y, int32_t num_ctas, void *stream) {
-    if (!W || !X || !Y || (!items && n_items > 0) || E < 1 || M < BM || K < BK || T < 1 || n_items < 0)
+METRO_API int32_t moe_item_tokens(void) { return kItemTokens; }
+
+METRO_API int moe_grouped_gemm_v2(const void *W, int32_t E, int32_t M, int32_t K, const void *X, int32_t T,
+                                  const int32_t *items, int32_t n_items, int32_t max_item_tokens, void *Y,
+                                  int32_t num_ctas, void *stream) {
+    if (!W || !X || !Y || (!items && n_items > 0) || E < 1 || M < BM || K < BK || T < 1 || n_items < 0 ||
+        max_item_tokens < 1 || max_item_tokens > MAXN)
         return METRO_EARG;
     if (M % BM || K % BK) return METRO_EDIMS;
     if (n_items == 0) return METRO_OK;
-    return launch_gemm(W, E, M, K, X, T, items, n_items, nullptr, Y, num_ctas, stream);
+    return launch_gemm(W, E, M, K, X, T, items, n_items, nullptr, max_item_tokens, Y, num_ctas, stream);
+}
+
+METRO_API int moe_grouped_gemm_v1(const void *W, int32_t E, int32_t M, int32_t K, const void *X, int32_t T,
+                        const int32_t *items, int32_t n_items, void *Y, int32_t num_ctas, void *stream) {
+    return moe_grouped_gemm_v2(W, E, M, K, X, T, items, n_items, MAXN, Y, num_ctas, stream);
+}
+
+METRO_API int moe_grouped_gemm_dev_v2(const void *W, int32_t E, int32_t M, int32_t K, const void *X,
+                                      int32_t T_cap, const int32_t *items, int32_t items_cap,
+                                      const int32_t *n_items_dev, int32_t max_item_tokens, void *Y, int32_t num_ctas,
+                                      void *stream) {
+    if (!W || !X || !Y || !items || !n_items_dev || E < 1 || M < BM || K < BK || T_cap < 1 || items_cap < 1 ||
+        max_item_tokens < 1 || max_item_tokens > MAXN)
+        return METRO_EARG;
+    if (M % BM || K % BK) return METRO_EDIMS;
+    return launch_gemm(W, E, M, K, X, T_cap, items, items_cap, n_items_dev, max_item_tokens, Y, num_ctas, stream);
 }
 
 METRO_API int moe_grouped_gemm_dev_v1(const void *W, int32_t E, int32_t M, int32_t K, const void *X,
                                       int32_t T_cap, const int32_t *items, int32_t items_cap,
                                       const int32_t *n_items_dev, void *Y, int32_t num_ctas, void *stream) {
-    if (!W || !X || !Y || !items || !n_items_dev || E < 1 || M < BM || K < BK || T_cap < 1 || items_cap < 1)
-        return METRO_EARG;
-    if (M % BM || K % BK) return METRO_EDIMS;
-    return launch_gemm(W, E, M, K, X, T_cap, items, items_cap, n_items_dev, Y, num_ctas, stream);
+    return moe_grouped_gemm_dev_v2(W, E, M, K, X, T_cap, items, items_cap, n_items_dev, MAXN, Y, num_ctas, stream);
 }
 
 METRO_API int moe_layout_items_v1(const int32_t *rep_off, const int32_t *slot_base, int32_t rank, int32_t M1,

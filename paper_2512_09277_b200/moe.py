@@ -22,7 +22,7 @@ from . import _native
 from .core import ValidationError
 
 BM = 128      # weight rows per tile
-MAXN = 256    # tokens per work item
+MAXN = 256    # tokens per work item (wide GEMM tiling; moe_item_tokens() for the items we build)
 
 
 def _lib():
@@ -33,6 +33,12 @@ def _lib():
         P, i32 = ctypes.c_void_p, ctypes.c_int32
         L.moe_grouped_gemm_v1.argtypes = [P, i32, i32, i32, P, i32, P, i32, P, i32, P]
         L.moe_grouped_gemm_v1.restype = ctypes.c_int
+        L.moe_grouped_gemm_v2.argtypes = [P, i32, i32, i32, P, i32, P, i32, i32, P, i32, P]
+        L.moe_grouped_gemm_v2.restype = ctypes.c_int
+        L.moe_grouped_gemm_dev_v2.argtypes = [P, i32, i32, i32, P, i32, P, i32, P, i32, P, i32, P]
+        L.moe_grouped_gemm_dev_v2.restype = ctypes.c_int
+        L.moe_item_tokens.argtypes = []
+        L.moe_item_tokens.restype = ctypes.c_int32
         L.moe_silu_mul_v1.argtypes = [P, i32, i32, P, P]
         L.moe_silu_mul_v1.restype = ctypes.c_int
         L.moe_grouped_gemm_dev_v1.argtypes = [P, i32, i32, i32, P, i32, P, i32, P, P, i32, P]
@@ -57,24 +63,42 @@ def _check(rc: int, what: str) -> None:
     raise ValidationError(f"{what}: {_lib().metro_strerror(rc).decode()}")
 
 
+def item_tokens() -> int:
+    """Tokens per work item of the items this package builds (build_items and
+    moe_layout_items_v1): the narrow, deeper-pipelined GEMM tiling."""
+    return int(_lib().moe_item_tokens())
+
+
 def build_items(groups: Sequence[Tuple[int, int, int]], M: int) -> np.ndarray:
     """Work items for groups of (expert slot e, first token row t0, token count n):
-    every 128-row block of W[e] x every <=256-token chunk of the group."""
+    every 128-row block of W[e] x every <= item_tokens() chunk of the group."""
     if M % BM:
         raise ValidationError(f"M={M} must be a multiple of {BM}")
     out = []
     for e, t0, n in groups:
         # token chunks of one weight block are adjacent, so the CTAs that run them
         # concurrently share the block's HBM read through L2
+        ch = item_tokens()
         for mb in range(M // BM):
-            for c0 in range(0, n, MAXN):
-                out.append((e, mb, t0 + c0, min(MAXN, n - c0)))
+            for c0 in range(0, n, ch):
+                out.append((e, mb, t0 + c0, min(ch, n - c0)))
     return np.asarray(out, dtype=np.int32).reshape(-1, 4)
 
 
-def grouped_gemm(W: torch.Tensor, X: torch.Tensor, items: torch.Tensor, Y: torch.Tensor = None,
-                 num_ctas: int = 0) -> torch.Tensor:
-    """Y[t, m] = sum_k W[e][m, k] X[t, k] for every item (bf16 in/out, fp32 accumulate)."""
+def grouped_gemm(W: torch.Tensor, X: torch.Tensor, items, Y: torch.Tensor = None,
+                 num_ctas: int = 0, max_item_tokens: int = None) -> torch.Tensor:
+    """Y[t, m] = sum_k W[e][m, k] X[t, k] for every item (bf16 in/out, fp32 accumulate).
+
+    ``max_item_tokens`` bounds the items' token counts: <= item_tokens() selects
+    the deeper-pipelined narrow tiling.  Taken from host items; device items
+    without it use the wide tiling (any count <= 256)."""
+    if max_item_tokens is None:
+        if isinstance(items, np.ndarray) or (isinstance(items, torch.Tensor) and not items.is_cuda):
+            a = np.asarray(items).reshape(-1, 4)
+            max_item_tokens = int(a[:, 3].max()) if len(a) else 1
+        else:
+            max_item_tokens = MAXN
+        items = torch.as_tensor(np.asarray(items).reshape(-1, 4) if isinstance(items, np.ndarray) else items)
     if W.dtype != torch.bfloat16 or X.dtype != torch.bfloat16:
         raise ValidationError("W and X must be bfloat16")
     if W.dim() != 3 or X.dim() != 2 or W.shape[2] != X.shape[1]:
@@ -84,10 +108,10 @@ def grouped_gemm(W: torch.Tensor, X: torch.Tensor, items: torch.Tensor, Y: torch
     items = items.to(device=W.device, dtype=torch.int32).contiguous()
     if Y is None:
         Y = torch.empty((T, M), dtype=torch.bfloat16, device=W.device)
-    rc = _lib().moe_grouped_gemm_v1(W.data_ptr(), E, M, K, X.data_ptr(), T, items.data_ptr(),
-                                    items.shape[0], Y.data_ptr(), num_ctas,
+    rc = _lib().moe_grouped_gemm_v2(W.data_ptr(), E, M, K, X.data_ptr(), T, items.data_ptr(),
+                                    items.shape[0], int(max_item_tokens), Y.data_ptr(), num_ctas,
                                     torch.cuda.current_stream(W.device).cuda_stream)
-    _check(rc, "moe_grouped_gemm_v1")
+    _check(rc, "moe_grouped_gemm_v2")
     return Y
 
 
@@ -157,9 +181,10 @@ class ExpertFFN:
                     torch.empty((T, self.inter), dtype=torch.bfloat16, device=X.device),
                     torch.empty((T, self.hidden), dtype=torch.bfloat16, device=X.device))
         GU, H, Y = bufs
-        grouped_gemm(self.W1, X, items1, GU)
+        nt = item_tokens()  # plan() builds items with build_items
+        grouped_gemm(self.W1, X, items1, GU, max_item_tokens=nt)
         silu_mul(GU, H)
-        grouped_gemm(self.W2, H, items2, Y)
+        grouped_gemm(self.W2, H, items2, Y, max_item_tokens=nt)
         return Y
 
 
@@ -191,7 +216,7 @@ class RankMoE:
             raise ValidationError(f"rank {rank} hosts {slots} experts but the FFN has {ffn.slots} slots")
         self.max_pairs = int(max_pairs)
         self.rows_cap = max(1, self.max_pairs)
-        chunks = slots + self.rows_cap // MAXN + 1
+        chunks = slots + self.rows_cap // item_tokens() + 1
         self.cap1 = chunks * (2 * ffn.inter // BM)
         self.cap2 = chunks * (ffn.hidden // BM)
         self.route_out = self.router.alloc(self.max_pairs, pair_rank=True, top_k=self.top_k)
@@ -236,14 +261,15 @@ class RankMoE:
                                     lo.pair_row.data_ptr(), P, self.rank, self.X.data_ptr(), self.rows_cap, sp),
                "moe_gather_rows_v1")
         f = self.ffn
-        _check(L.moe_grouped_gemm_dev_v1(f.W1.data_ptr(), f.slots, 2 * f.inter, f.hidden, self.X.data_ptr(),
+        nt = item_tokens()  # moe_layout_items_v1 chunks at this many tokens
+        _check(L.moe_grouped_gemm_dev_v2(f.W1.data_ptr(), f.slots, 2 * f.inter, f.hidden, self.X.data_ptr(),
                                          self.rows_cap, self.items1.data_ptr(), self.cap1,
-                                         self.counts.data_ptr(), self.GU.data_ptr(), 0, sp),
-               "moe_grouped_gemm_dev_v1")
+                                         self.counts.data_ptr(), nt, self.GU.data_ptr(), 0, sp),
+               "moe_grouped_gemm_dev_v2")
         _check(L.moe_silu_mul_dev_v1(self.GU.data_ptr(), self.rows_cap, f.inter, self.H.data_ptr(),
                                      self.counts[2:].data_ptr(), sp), "moe_silu_mul_dev_v1")
-        _check(L.moe_grouped_gemm_dev_v1(f.W2.data_ptr(), f.slots, f.hidden, f.inter, self.H.data_ptr(),
+        _check(L.moe_grouped_gemm_dev_v2(f.W2.data_ptr(), f.slots, f.hidden, f.inter, self.H.data_ptr(),
                                          self.rows_cap, self.items2.data_ptr(), self.cap2,
-                                         self.counts[1:].data_ptr(), self.Y.data_ptr(), 0, sp),
-               "moe_grouped_gemm_dev_v1")
+                                         self.counts[1:].data_ptr(), nt, self.Y.data_ptr(), 0, sp),
+               "moe_grouped_gemm_dev_v2")
         return self.Y

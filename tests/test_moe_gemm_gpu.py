@@ -48,6 +48,40 @@ def test_grouped_gemm_vs_torch(E, M, K, sizes):
     torch.testing.assert_close(Y.float(), ref_gemm(W, X, groups), rtol=RTOL, atol=ATOL)
 
 
+def wide_items(groups, M, chunk=256):
+    """Items chunked at up to 256 tokens (the wide tiling), built here independently."""
+    out = []
+    for e, t0, n in groups:
+        for mb in range(M // moe.BM):
+            for c0 in range(0, n, chunk):
+                out.append((e, mb, t0 + c0, min(chunk, n - c0)))
+    return np.asarray(out, dtype=np.int32).reshape(-1, 4)
+
+
+@pytest.mark.parametrize("chunk", [64, 128, 256])
+def test_grouped_gemm_both_tilings(chunk):
+    """Narrow (<= item_tokens() per item, 8-stage ring) and wide (<= 256, 4 stages)
+    tilings on the same problem; device-resident items without a hint take the
+    wide tiling, host items pick by their largest token count."""
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(chunk)
+    E, M, K = 3, 384, 1024
+    sizes = [1, 63, 64, 65, 200, 256, 300]
+    groups, t = [], 0
+    for i, n in enumerate(sizes):
+        groups.append((i % E, t, n))
+        t += n
+    W = (torch.randn((E, M, K), generator=g, device=dev) * K ** -0.5).to(torch.bfloat16)
+    X = torch.randn((t, K), generator=g, device=dev).to(torch.bfloat16)
+    items = wide_items(groups, M, chunk)
+    ref = ref_gemm(W, X, groups)
+    for it in (items, torch.from_numpy(items).to(dev)):
+        Y = moe.grouped_gemm(W, X, it)
+        torch.cuda.synchronize()
+        torch.testing.assert_close(Y.float(), ref, rtol=RTOL, atol=ATOL)
+    assert moe.item_tokens() == 64
+
+
 def test_grouped_gemm_few_ctas_many_items():
     """More items than CTAs: the persistent loop, TMEM double buffering and the
     smem ring wrap many times."""
