@@ -1,23 +1,28 @@
 #!/usr/bin/env bash
 # Collect the ncu evidence committed under profiles/ (run ON the GPU box, 1 GPU):
-#   1. launch list of the bench command (device time per launch, cold-cache, serialised)
-#   2. one `ncu --set full` capture of the routing kernel (DeepSeek-V3 shape)
-#   3. one `ncu --set full` capture of the K3 grouped GEMM (gate_up projection)
+#   1. launch list of a short bench run (device time per launch, cold-cache, serialised)
+#   2. `ncu --set full` captures of the routing kernel (DeepSeek-V3 shape), the K3
+#      grouped GEMM (gate_up of the bottleneck rank), the fused gating kernel, the
+#      dispatch layout kernel and the fused exchange kernel (world 1)
 # Then, in the build container: python tools/summarize_profiles.py <round>
-set -euo pipefail
+set -uo pipefail
 OUT=${1:-gpurun_out}
 mkdir -p "$OUT"
 NCU="ncu --clock-control none"
 
-# 1. launch list (first 400 launches of a short bench run; the pool graphs are big)
-$NCU --metrics gpu__time_duration.sum -c 400 --csv --log-file "$OUT/launches.csv" \
-    python bench.py --steps 256 --warmup 3 --e2e-steps 20 --cpu-seconds 0.2 --no-moe > "$OUT/launches_bench.log" 2>&1 || true
+$NCU --metrics gpu__time_duration.sum -k regex:metro_ids_kernel -c 300 --csv --log-file "$OUT/launches.csv" \
+    python bench.py --steps 256 --warmup 3 --e2e-steps 20 --cpu-seconds 0.2 --no-moe > "$OUT/launches_bench.log" 2>&1
+$NCU --metrics gpu__time_duration.sum -c 400 --csv --log-file "$OUT/launches_all.csv" \
+    python bench.py --steps 256 --warmup 3 --e2e-steps 20 --cpu-seconds 0.2 --no-moe > /dev/null 2>&1
 
-# 2. full capture of the routing kernel (skip warm-up launches)
-$NCU --set full --import-source on -k regex:metro_ids_kernel -s 5 -c 1 -o "$OUT/metro_full" \
-    python tools/profile_target.py metro > "$OUT/metro_full.log" 2>&1 || true
-
-# 3. full capture of K3 (first grouped GEMM launch = gate_up of the METRO rank)
-$NCU --set full --import-source on -k regex:moe_gemm -c 1 -o "$OUT/moe_full" \
-    python tools/moe_layer_bench.py --batches 1 --reps 1 > "$OUT/moe_full.log" 2>&1 || true
+full() {  # name, kernel regex, skip, command...
+    local name=$1 kre=$2 skip=$3; shift 3
+    $NCU --set full --import-source on -k "regex:$kre" -s "$skip" -c 1 -o "$OUT/${name}_full" "$@" \
+        > "$OUT/${name}_full.log" 2>&1
+}
+full metro metro_ids_kernel 5 python tools/profile_target.py metro
+full moe moe_gemm 0 python tools/moe_layer_bench.py --batches 1 --reps 1
+full gate 'metro_(gate|ids)_kernel' 5 python tools/profile_target.py gate
+full dispatch layout_kernel 5 python tools/profile_target.py dispatch
+full exchange metro_allgather_kernel 5 python tools/profile_target.py exchange
 ls -la "$OUT"

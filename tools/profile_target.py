@@ -1,7 +1,10 @@
 """Minimal launch sequences for ncu captures (no graphs, few launches).
 
-    python tools/profile_target.py metro   # 8 routing launches, DeepSeek-V3 shape (B=1024)
-    python tools/profile_target.py eplb    # 8 EPLB launches, same inputs
+    python tools/profile_target.py metro [B]     # 8 routing launches, DeepSeek-V3 shape
+    python tools/profile_target.py eplb [B]      # 8 EPLB launches, same inputs
+    python tools/profile_target.py gate [B]      # 8 fused gating top-k + METRO launches (fp32 scores)
+    python tools/profile_target.py dispatch [B]  # 8 dispatch-layout launches behind METRO routing
+    python tools/profile_target.py exchange [B]  # 8 fused exchange + route launches, world 1
 """
 
 import os
@@ -10,7 +13,8 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2512_09277_b200 import DevicePlacement, Router  # noqa: E402
+from paper_2512_09277_b200 import DevicePlacement, DispatchLayout, Router  # noqa: E402
+from paper_2512_09277_b200.dist import virtual_ranks  # noqa: E402
 from paper_2512_09277_b200.placement import gen_zipf_topk, make_placement  # noqa: E402
 
 
@@ -20,12 +24,33 @@ def main():
     dev = torch.device("cuda", 0)
     A = make_placement(256, 8, 1.5, 7).matrix
     pl = DevicePlacement(A, dev)
-    r = Router(pl, "metro" if what == "metro" else "eplb")
     batches = [torch.from_numpy(gen_zipf_topk(256, 8, B, 1.2, 1000 + s, popularity_seed=7)).to(dev)
                for s in range(8)]
-    out = r.alloc(B * 8, top_k=8)
-    for b in batches:
-        r.route(b, out=out)
+    if what in ("metro", "eplb"):
+        r = Router(pl, what)
+        out = r.alloc(B * 8, top_k=8)
+        for b in batches:
+            r.route(b, out=out)
+    elif what == "gate":
+        r = Router(pl, "metro")
+        g = torch.Generator(device=dev).manual_seed(3)
+        scores = [torch.randn((B, 256), generator=g, device=dev) for _ in range(8)]
+        for sc in scores:
+            r.route_scores(sc, 8)
+    elif what == "dispatch":
+        r = Router(pl, "metro")
+        lay = DispatchLayout(pl)
+        out = r.alloc(B * 8, top_k=8)
+        for b in batches:
+            r.route(b, out=out)
+            lay(b.reshape(-1), out.pair_rank)
+    elif what == "exchange":
+        routers, bufs = virtual_ranks(pl, 1, B, 8)
+        for b in batches:
+            routers[0].step(b)
+        torch.cuda.synchronize()
+        for x in bufs:
+            x.close()
     torch.cuda.synchronize()
     print("ok", what, B)
 

@@ -12,7 +12,7 @@ import subprocess
 import sys
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SRC = os.path.join(REPO, "gpurun_out")
+SRC = os.environ.get("PROFILE_SRC") or os.path.join(REPO, "gpurun_out")
 DST = os.path.join(REPO, "profiles")
 
 KEYS = [
@@ -50,7 +50,9 @@ def main():
     rnd = sys.argv[1] if len(sys.argv) > 1 else "r1"
     os.makedirs(DST, exist_ok=True)
     traffic = {}
-    for name, rep in (("metro", "metro_full.ncu-rep"), ("moe_gemm", "moe_full.ncu-rep")):
+    for name, rep in (("metro", "metro_full.ncu-rep"), ("moe_gemm", "moe_full.ncu-rep"),
+                      ("gate", "gate_full.ncu-rep"), ("dispatch", "dispatch_full.ncu-rep"),
+                      ("exchange", "exchange_full.ncu-rep")):
         path = os.path.join(SRC, rep)
         if not os.path.exists(path):
             continue
@@ -67,9 +69,8 @@ def main():
         with open(os.path.join(DST, "ncu_traffic.json"), "w") as f:
             json.dump({"ds": traffic["metro"], "source": f"{rnd}_metro_ncu_full.txt (dram read+write bytes, "
                        "one launch, DeepSeek-V3 shape B=1024)", "moe_gemm": traffic.get("moe_gemm")}, f, indent=1)
-    lp = os.path.join(SRC, "launches.csv")
-    if os.path.exists(lp):
-        rows = [r for r in csv.reader(open(lp)) if len(r) > 5]
+    def launch_table(path, title):
+        rows = [r for r in csv.reader(open(path)) if len(r) > 5]
         hdr = rows[0]
         kn, mv = hdr.index("Kernel Name"), hdr.index("Metric Value")
         tot = {}
@@ -78,14 +79,26 @@ def main():
                 continue
             k = r[kn].split("(")[0][:60]
             v = float(r[mv].replace(",", ""))
-            n, s = tot.get(k, (0, 0.0))
-            tot[k] = (n + 1, s + v)
+            n, t = tot.get(k, (0, 0.0))
+            tot[k] = (n + 1, t + v)
+        lines = [title, "# cold-cache, serialised launches: compare SHARES, not absolute times (ns)"]
+        allt = sum(t for _, t in tot.values()) or 1.0
+        for k, (n, t) in sorted(tot.items(), key=lambda x: -x[1][1]):
+            lines.append(f"{k:62s} launches {n:5d}  mean {t / n:10.2f}  share {100 * t / allt:5.1f}%")
+        return lines
+
+    out = []
+    lp = os.path.join(SRC, "launches.csv")
+    if os.path.exists(lp):
+        out += launch_table(lp, "# ncu --metrics gpu__time_duration.sum --clock-control none -k regex:metro_ids_kernel "
+                                "(bench.py --steps 256: the timed region launches only this kernel)")
+    la = os.path.join(SRC, "launches_all.csv")
+    if os.path.exists(la):
+        out += [""] + launch_table(la, "# same command, first 400 launches of any kernel (incl. the bench's "
+                                       "one-time pool construction before the timed region)")
+    if out:
         with open(os.path.join(DST, f"{rnd}_launches_summary.txt"), "w") as f:
-            f.write("# ncu --metrics gpu__time_duration.sum --clock-control none (bench.py, first 400 launches)\n")
-            f.write("# cold-cache, serialised launches: compare SHARES, not absolute times\n")
-            allt = sum(s for _, s in tot.values())
-            for k, (n, s) in sorted(tot.items(), key=lambda x: -x[1][1]):
-                f.write(f"{k:62s} launches {n:5d}  mean {s / n:10.2f}  share {100 * s / allt:5.1f}%\n")
+            f.write("\n".join(out) + "\n")
     print("wrote", sorted(os.listdir(DST)))
 
 
