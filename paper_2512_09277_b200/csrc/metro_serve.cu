@@ -133,7 +133,8 @@ __global__ void __launch_bounds__(kServeThreads, 1)
                        uint32_t stagger) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31;
-    const Layout L = make_layout(kMetroIds, base.N, W, 1, base.slice, base.C, 1);
+    const Layout L = make_layout(kMetroIds, base.N, W, 1, base.slice, base.C, base.staged);
+    const bool staged = base.staged != 0;
     ServeReq &rq = *reinterpret_cast<ServeReq *>(smem + align_up(L.total, 16));
 
     if (tid >= kThreads) {
@@ -259,7 +260,7 @@ __global__ void __launch_bounds__(kServeThreads, 1)
                 for (int u = 0; u < U; ++u) {
                     const int i = i0 + u * kThreads;
                     if (i < n4) {
-                        reinterpret_cast<int4 *>(s_ids)[i] = v[u];
+                        if (staged) reinterpret_cast<int4 *>(s_ids)[i] = v[u];
                         const int ev[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(kServeThreads, 1)
             }
             for (int i = n4 * 4 + tid; i < n; i += kThreads) {
                 const int e = ld_relaxed_sys_s32(p.ids + i);
-                s_ids[i] = e;
+                if (staged) s_ids[i] = e;
                 if (static_cast<unsigned>(e) < static_cast<unsigned>(p.N))
                     atomicAdd(&s_hist[e * p.C + (lane & cm)], 1);
                 else
@@ -294,12 +295,14 @@ __global__ void __launch_bounds__(kServeThreads, 1)
             const int32_t *s_choice = reinterpret_cast<const int32_t *>(smem + L.choice);
             if (p.pair_rank) {
                 const int n4 = n >> 2;
+                const int4 *src4 = reinterpret_cast<const int4 *>(p.ids);
                 for (int i = tid; i < n4; i += kThreads) {
-                    const int4 v = reinterpret_cast<const int4 *>(s_ids)[i];
+                    const int4 v = staged ? reinterpret_cast<const int4 *>(s_ids)[i] : ld_relaxed_sys_v4(src4 + i);
                     reinterpret_cast<int4 *>(p.pair_rank)[i] =
                         make_int4(s_choice[v.x], s_choice[v.y], s_choice[v.z], s_choice[v.w]);
                 }
-                for (int i = n4 * 4 + tid; i < n; i += kThreads) p.pair_rank[i] = s_choice[s_ids[i]];
+                for (int i = n4 * 4 + tid; i < n; i += kThreads)
+                    p.pair_rank[i] = s_choice[staged ? s_ids[i] : ld_relaxed_sys_s32(p.ids + i)];
             }
             for (int e = tid; e < p.N; e += kThreads) p.choice[e] = s_choice[e];
             if (tid == 0) {
@@ -339,18 +342,21 @@ __global__ void __launch_bounds__(kServeThreads, 1)
 static int serve_plan(int N, int W, int64_t max_pairs, Params &p) {
     int64_t slice = (max_pairs + 3) & ~int64_t(3);
     if (slice < 4) slice = 4;
-    int C = 32;
-    while (C > 1 && N * C * 4 > 64 * 1024) C >>= 1;
-    for (; C >= 1; C >>= 1) {
-        const Layout L = make_layout(kMetroIds, N, W, 1, slice, C, 1);
-        const int total = align_up(L.total, 16) + static_cast<int>(sizeof(ServeReq));
-        if (total <= kMaxSmem) {
-            p.slice = slice;
-            p.staged = 1;
-            p.C = C;
-            return total;
+    int C0 = 32;
+    while (C0 > 1 && N * C0 * 4 > 64 * 1024) C0 >>= 1;
+    // staged: the whole batch in shared memory; otherwise (batches beyond ~40k
+    // pairs) the ids are read from host memory a second time for the pair ranks
+    for (int staged = 1; staged >= 0; --staged)
+        for (int C = C0; C >= 1; C >>= 1) {
+            const Layout L = make_layout(kMetroIds, N, W, 1, slice, C, staged);
+            const int total = align_up(L.total, 16) + static_cast<int>(sizeof(ServeReq));
+            if (total <= kMaxSmem) {
+                p.slice = slice;
+                p.staged = staged;
+                p.C = C;
+                return total;
+            }
         }
-    }
     return METRO_EDIMS;
 }
 

@@ -46,9 +46,9 @@ def check(sr, ids, A):
 
 
 def test_served_golden_shapes(shapes):
+    # batches up to 32k pairs are staged in shared memory; B = 8192 (65,536 pairs)
+    # reads the ids from host memory a second time for the pair ranks
     for c in shapes:
-        if c["B"] * c["k"] > 32768:  # the whole batch is staged in one CTA
-            continue
         pl = DevicePlacement(c["A"])
         with ServedRouter(pl, c["B"] * c["k"]) as sr:
             check(sr, c["ids"], c["A"])
