@@ -110,16 +110,16 @@ struct ServeReq {
 };
 
 // Thread roles.  Warps 0..15 (kThreads) route, with the named barrier 1 of
-// metro_core.cuh (cta_sync).  Warps 16..16+kDoorbellWarps-1 only poll: lane 0
+// metro_core.cuh (cta_sync).  Warps 16.. (1-4 of them, default 2) only poll: lane 0
 // of each keeps one system-scope acquire load of the doorbell in flight, the
 // warps started `stagger` ns apart, so a doorbell load reaches host memory every
-// ~RTT / kDoorbellWarps.  The first to see a new request claims it and arrives
+// ~RTT / (doorbell warps).  The first to see a new request claims it and arrives
 // on barrier 2 (the routing warps sync on it): the routing warps never wait for
 // the other pollers' loads still in flight.  Barrier 3 (everyone) closes a
 // request.  Acquire loads + barrier give the formal order: the routing warps'
 // id loads happen after the doorbell load that saw the request.
-constexpr int kDoorbellWarps = 4;
-constexpr int kServeThreads = kThreads + 32 * kDoorbellWarps;
+constexpr int kMaxDoorbellWarps = 4;
+constexpr int kServeThreads = kThreads + 32 * kMaxDoorbellWarps;  // launch bound; the launch may use fewer
 enum FenceMode { kFenceRelease = 0, kFenceOne = 1, kFenceAll = 2 };
 
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -137,13 +137,14 @@ __global__ void __launch_bounds__(kServeThreads, 1)
     const bool staged = base.staged != 0;
     ServeReq &rq = *reinterpret_cast<ServeReq *>(smem + align_up(L.total, 16));
 
+    const int nthreads = static_cast<int>(blockDim.x);  // kThreads + 32 x doorbell warps
     if (tid >= kThreads) {
         // ================= doorbell warps
         const int d = (tid - kThreads) >> 5;
         volatile ServeReq &vrq = rq;
         uint64_t t_wait = globaltimer_ns();
         for (uint32_t epoch = 1;; ++epoch) {
-            bar_sync(3, kServeThreads);  // the previous request is closed
+            bar_sync(3, nthreads);  // the previous request is closed
             int won = 0;
             if (lane == 0) {
                 if (d) __nanosleep(d * stagger);
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(kServeThreads, 1)
         // ---- per-request state, cleared before the doorbell warps are released
         init_misc(misc);
         zero_smem(smem, L.aux, L.part);  // forced counts + histogram
-        bar_sync(3, kServeThreads);
+        bar_sync(3, nthreads);
         bar_sync(2, kThreads + 32);  // a doorbell warp claimed a request (or stop / idle)
         if (rq.verdict) {
             if (tid == 0) st_release_sys(&ctl->state, rq.verdict == 1 ? kServeStopped : kServeIdleExit);
@@ -372,8 +373,8 @@ struct metro_server {
     int W = 1, smem = 0;
     uint64_t idle_ns = 0;
     uint32_t seq = 0;
-    int fence_mode = 0;
-    uint32_t stagger = 500;
+    int fence_mode = 0, doorbell_warps = 2;
+    uint32_t stagger = 1000;
     bool sent_ptrs = false;
     int64_t max_pairs = 0, launches = 0;
     const void *ok_ids = nullptr, *ok_out = nullptr, *ok_pr = nullptr;
@@ -398,10 +399,10 @@ static int serve_launch(metro_server *s) {
     __atomic_store_n(&s->ctl->state, kServeLaunched, __ATOMIC_RELEASE);
     const uint32_t seq0 = s->seq;  // the last request this server completed
     switch (s->W) {
-        case 1: metro_serve_kernel<1><<<1, kServeThreads, s->smem, s->stream>>>(s->base, s->ctl, seq0, s->idle_ns, s->fence_mode, s->stagger); break;
-        case 2: metro_serve_kernel<2><<<1, kServeThreads, s->smem, s->stream>>>(s->base, s->ctl, seq0, s->idle_ns, s->fence_mode, s->stagger); break;
-        case 3: metro_serve_kernel<3><<<1, kServeThreads, s->smem, s->stream>>>(s->base, s->ctl, seq0, s->idle_ns, s->fence_mode, s->stagger); break;
-        case 4: metro_serve_kernel<4><<<1, kServeThreads, s->smem, s->stream>>>(s->base, s->ctl, seq0, s->idle_ns, s->fence_mode, s->stagger); break;
+        case 1: metro_serve_kernel<1><<<1, kThreads + 32 * s->doorbell_warps, s->smem, s->stream>>>(s->base, s->ctl, seq0, s->idle_ns, s->fence_mode, s->stagger); break;
+        case 2: metro_serve_kernel<2><<<1, kThreads + 32 * s->doorbell_warps, s->smem, s->stream>>>(s->base, s->ctl, seq0, s->idle_ns, s->fence_mode, s->stagger); break;
+        case 3: metro_serve_kernel<3><<<1, kThreads + 32 * s->doorbell_warps, s->smem, s->stream>>>(s->base, s->ctl, seq0, s->idle_ns, s->fence_mode, s->stagger); break;
+        case 4: metro_serve_kernel<4><<<1, kThreads + 32 * s->doorbell_warps, s->smem, s->stream>>>(s->base, s->ctl, seq0, s->idle_ns, s->fence_mode, s->stagger); break;
         default: return METRO_EDIMS;
     }
     e = cudaGetLastError();
@@ -431,6 +432,8 @@ int metro_server_create_v1(const uint32_t *mask, int32_t N, int32_t G, int64_t m
     s->base.G = G;
     {
         const char *f = getenv("METRO_SERVE_FENCE");  // tuning: "one" | "all" add fence.sc.sys
+        const char *dw = getenv("METRO_SERVE_DOORBELL_WARPS");  // tuning: 1..4 polling warps
+        if (dw) s->doorbell_warps = atoi(dw) < 1 ? 1 : (atoi(dw) > kMaxDoorbellWarps ? kMaxDoorbellWarps : atoi(dw));
         const char *st = getenv("METRO_SERVE_STAGGER_NS");  // tuning: doorbell load spacing
         if (st) s->stagger = static_cast<uint32_t>(atoi(st));
         s->fence_mode = !f ? kFenceRelease : strcmp(f, "all") == 0 ? kFenceAll : strcmp(f, "one") == 0 ? kFenceOne

@@ -61,15 +61,15 @@ int main() {
         });
     }
     // persistent server (metro_serve.h): both fence variants
-    struct Var { const char *name, *fence, *stagger; };
+    struct Var { const char *name, *warps, *stagger; };
     const Var vars[] = {
-        {"served release/st500", "release", "500"}, {"served release/st250", "release", "250"},
-        {"served release/st1000", "release", "1000"}, {"served one/st500", "one", "500"},
-        {"served all/st500", "all", "500"},
+        {"served 4 pollers st500", "4", "500"}, {"served 4 pollers st1000", "4", "1000"},
+        {"served 2 pollers st700", "2", "700"}, {"served 2 pollers st1000", "2", "1000"},
+        {"served 2 pollers st1500", "2", "1500"}, {"served 1 poller", "1", "0"},
     };
     for (const Var &v : vars) {
-        setenv("METRO_SERVE_FENCE", v.fence, 1);
         setenv("METRO_SERVE_STAGGER_NS", v.stagger, 1);
+        setenv("METRO_SERVE_DOORBELL_WARPS", v.warps, 1);
         for (int np : {P, 0}) {
             metro_server *srv = nullptr;
             int rc = metro_server_create_v1(dmask, N, G, P, 500000, &srv);
