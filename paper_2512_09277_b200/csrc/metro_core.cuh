@@ -473,14 +473,15 @@ __device__ __forceinline__ void packed_entry(uint32_t *dst, int r, uint32_t m, i
 // [n2, n2 + n3) r=3, [n2 + n3, m2) r>=4.  Slots up to m2 + 8 are readable (the
 // r=2 prefetch may touch them; they are never applied).
 __device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t *ent, const uint32_t *dlt, int n2,
-                                                 int n3, int m2, uint8_t *dec, PackedL L) {
-    uint8_t dec_s = 0;
+                                                 int n3, int m2, int32_t *choice, PackedL L) {
+    // every step stores its expert's choice (off the dependency chain: the store
+    // only reads the decision)
     auto step2 = [&](const uint4 &a, const uint4 &b) {
         const uint32_t va = prmt(L.lo, a.x, L.hi), vb = prmt(L.lo, a.y, L.hi);
         const uint32_t m = sgn(vb - va);
         L.lo += pick(a.z, b.x, m);
         L.hi += pick(a.w, b.y, m);
-        dec_s = static_cast<uint8_t>(m);  // decision only: choices are written in parallel later
+        choice[b.w] = static_cast<int32_t>((b.z >> (m & 8u)) & 0xffu);
     };
     // Four consecutive r=2 steps in one dependency chain.  All eight candidate loads
     // are extracted from the same L; step j corrects its difference by
@@ -488,7 +489,7 @@ __device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t
     // steps, each term a precomputed constant per hypothesis picked by step i's
     // mask (delta block: {dA, dA ^ dB} for the pairs 01 02 03 12 13 23).  The chain
     // per step is pick -> add -> sgn (~3 ops) instead of the full single-step chain.
-    auto block4 = [&](const uint4 (&a)[4], const uint4 (&b)[4], const uint4 (&d)[3]) -> uint32_t {
+    auto block4 = [&](const uint4 (&a)[4], const uint4 (&b)[4], const uint4 (&d)[3]) {
         uint32_t va[4], vb[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -515,8 +516,8 @@ __device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t
         }
         L.lo += ilo;
         L.hi += ihi;
-        // the four decisions as one word (byte i = step i's mask): choices later
-        return prmt(prmt(m0, 0x0040u, m1), 0x5410u, prmt(m2, 0x0040u, m3));
+#pragma unroll
+        for (int i = 0; i < 4; ++i) choice[b[i].w] = static_cast<int32_t>((b[i].z >> (m[i] & 8u)) & 0xffu);
     };
     int s = 0;
     if (n2 >= 4) {
@@ -539,7 +540,7 @@ __device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t
             }
 #pragma unroll
             for (int i = 0; i < 3; ++i) dn[i] = lds4(nd + i * 4);
-            reinterpret_cast<uint32_t *>(dec)[s >> 2] = block4(a, b, d);
+            block4(a, b, d);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 a[i] = an[i];
@@ -549,10 +550,7 @@ __device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t
             for (int i = 0; i < 3; ++i) d[i] = dn[i];
         }
     }
-    for (; s < n2; ++s) {
-        step2(lds4(ent + s * kES), lds4(ent + s * kES + 4));
-        dec[s] = dec_s;
-    }
+    for (; s < n2; ++s) step2(lds4(ent + s * kES), lds4(ent + s * kES + 4));
     stamp(p, 8);
     // r = 3 steps, next entry prefetched (slots past m2 stay readable)
     if (s < n2 + n3) {
@@ -567,7 +565,9 @@ __device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t
             const uint32_t m2v = sgn(vc - vab);
             L.lo += pick(ilo, ilo ^ c.x, m2v);
             L.hi += pick(ihi, ihi ^ c.y, m2v);
-            dec[s] = static_cast<uint8_t>((m1 & 1u) | (m2v & 2u));  // b beat a | c won
+            // winner: c if it beat the a/b winner, else b if it beat a, else a
+            const uint32_t sh = (m2v & 16u) | (~m2v & m1 & 8u);
+            choice[c.w] = static_cast<int32_t>((c.z >> sh) & 0xffu);
             a = an;
             b = bn;
             c = cn;
@@ -579,8 +579,10 @@ __device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t
     // Next entry prefetched.
     if (s < m2) {
         uint4 n0 = lds4(ent + s * kES), n1 = lds4(ent + s * kES + 4);
+        uint32_t id = ent[s * kES + 8];
         for (; s < m2; ++s) {
             const uint4 q0 = lds4(ent + (s + 1) * kES), q1 = lds4(ent + (s + 1) * kES + 4);
+            const uint32_t qid = ent[(s + 1) * kES + 8];
             const uint32_t c[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
             uint32_t k[8];
 #pragma unroll
@@ -589,9 +591,10 @@ __device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t
             const uint32_t sh = kmin & 0x38u;
             L.lo += shl_clamp(1u, sh);
             L.hi += shl_clamp(1u, sh - 32u);
-            dec[s] = static_cast<uint8_t>(sh);
+            choice[id] = static_cast<int32_t>(sh >> 3);
             n0 = q0;
             n1 = q1;
+            id = qid;
         }
     }
     stamp(p, 10);
@@ -769,8 +772,6 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
     stamp(p, 5);
 
     bool done = false;
-    // per-step decisions of the packed r=2/3 steps (the key array is dead by now)
-    uint8_t *s_dec = smem + L.keys;
     if (MODE != kFromOrder && try_packed) {
         // Packed greedy (thread 0).  Valid iff every final counter is <= 126: the
         // counters only grow, so no byte ever crossed into the sign bit.
@@ -790,7 +791,7 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
             const int n2 = misc[M_N2], n3 = misc[M_N3] - n2;
             if (ok)
                 Lp = packed_greedy(p, s_ent, reinterpret_cast<const uint32_t *>(smem + L.rpart), n2, n3, m2,
-                                   s_dec, Lp);
+                                   s_choice, Lp);
             // every final counter <= 126 (no byte reached the sign bit; counters only
             // grow) and the byte sum equals the assignments (no byte wrapped past 255)
             ok = ok && ((Lp.lo | Lp.hi) & 0x80808080u) == 0 && ((Lp.lo + 0x01010101u) & 0x80808080u) == 0 &&
@@ -809,22 +810,7 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
         }
         cta_sync();
         done = misc[M_PACKED_OK] != 0;
-        if (done) {
-            // choices of the r=2/3 steps from their decision bytes, off the serial chain
-            const int n2 = misc[M_N2], n23 = misc[M_N3];
-            for (int q = tid; q < m2; q += kThreads) {
-                const uint32_t d = s_dec[q];
-                const uint32_t *en = s_ent + q * kES;
-                if (q >= n23) {  // r >= 4: d = 8 * winner
-                    s_choice[en[8]] = static_cast<int32_t>(d >> 3);
-                    continue;
-                }
-                const bool three = q >= n2;
-                const uint32_t gs = three ? en[10] : en[6];
-                const uint32_t sh = (three && (d & 2u)) ? 16u : ((d & 1u) ? 8u : 0u);
-                s_choice[three ? en[11] : en[7]] = static_cast<int32_t>((gs >> sh) & 0xffu);
-            }
-            cta_sync();
+        if (done) {  // the greedy thread stored every choice as it went
             stamp(p, 6);
             return true;
         }
