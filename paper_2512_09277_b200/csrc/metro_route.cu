@@ -7,24 +7,26 @@
 //     _greedy_assign routing.py:90-102  argmin L over ascending replicas, strict '<'
 //   route_eplb       routing.py:55-72   even split, remainder to low rank ids
 //
-// Kernel structure.  One thread-block cluster of R CTAs routes
-// one layer; the path is a latency chain, so every phase is shaped to keep
-// memory latency off it:
+// Kernel structure (device phases in metro_core.cuh).  One
+// thread-block cluster of R CTAs routes one layer; the path is a latency chain,
+// so every phase is shaped to keep memory latency off it:
+//   (0) programmatic dependent launch: the shared-memory prologue runs while the
+//       previous kernel in the stream finishes; griddepcontrol.wait precedes the
+//       first global access;
 //   (A) thread 0 issues the TMA bulk copies (cp.async.bulk + mbarrier) of the rank
-//       bitmasks and of this CTA's contiguous id slice as its first instruction;
+//       bitmasks and of this CTA's contiguous id slice;
 //   (B) the slice is histogrammed into lane-striped shared counters hist[e][lane]
 //       (each lane owns a bank: hot experts never serialise a warp's atomics);
-//   (C) each expert's 32 lane counters are summed with bank-rotated 128-bit loads
-//       and the partial is stored straight into every peer CTA's shared memory
-//       (DSMEM st.shared::cluster) -- ONE cluster barrier completes the exchange;
-//   (D) every CTA redundantly (no second barrier) sums the partials into T and
+//   (C) each expert's lane counters are summed with bank-rotated 128-bit loads and
+//       the CTA's partial row is shipped to every peer CTA with 16-byte st.async
+//       stores that complete bytes on the receiver's mbarrier (no cluster barrier);
+//   (D) every CTA redundantly (no second exchange) sums the partials into T and
 //       classifies experts in the same pass: single-replica experts are applied
-//       as an order-free prefix (per-rank ballots), replicated ones are
-//       stream-compacted, rank-sorted by the canonical key with broadcast loads,
-//       and the serial greedy runs in ONE warp: lane g owns L[g] packed as
-//       (L << 8 | g); the candidacy bits of 32 steps are transposed into
-//       registers with ballots, so each step is SEL -> redux.sync.min -> compare ->
-//       add with no memory access on the dependency chain;
+//       as an order-free prefix, replicated ones are stream-compacted and
+//       rank-sorted by the canonical key with broadcast loads; the serial greedy
+//       runs predicate-free in ONE thread on byte-packed counters for G <= 8
+//       (blocks of four r = 2 steps with precomputed corrections), else in one
+//       warp (lane g owns L[g] << 8 | g; SEL -> redux.sync.min -> compare -> add);
 //   (E) each CTA writes pair_rank for its own slice from shared memory; CTA 0
 //       writes loads / choice / rank_counts / lam / status.
 #include <cuda_runtime.h>
@@ -538,8 +540,17 @@ template <typename K, typename... Args>
 static cudaError_t launch_plain(K kernel, int grid, int smem, cudaStream_t s, Args... args) {
     cudaError_t e = prepare(kernel);
     if (e != cudaSuccess) return e;
-    kernel<<<grid, kThreads, smem, s>>>(args...);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // griddep_wait before global access
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 static int words_for(int G) { return (G + 31) / 32; }
