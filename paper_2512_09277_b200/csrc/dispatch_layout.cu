@@ -54,15 +54,18 @@ struct Params {
     int32_t *pair_row;
     int32_t *rep_off;
     int32_t *status;
+    int32_t rtab_smem;  // 1: the replica table is staged in shared memory
 };
 
 // smem: bad (8) | cta_tot [nrep + 1] | pre [nrep] | loc [nrep + 1] | off [nrep + 1] | sb [G + 1] | wsum [32] |
-//       hw [kWarps][nrep] | pk [slice]   (pk = rid << 16 | in-warp rank)
+//       hw [kWarps][nrep] | pk [slice] | rtab [N * G] (optional) | base [nrep] | e [slice] | g [slice]
+//       (pk = rid << 16 | in-warp rank; rtab = the replica table staged once;
+//        base[rid] = first row offset of rid's rank)
 struct Layout {
-    int bad, tot, pre, loc, off, sb, wsum, hw, pk, total;
+    int bad, tot, pre, loc, off, sb, wsum, hw, pk, rtab, base, se, sg, total;
 };
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
-__host__ __device__ inline Layout make_layout(int nrep, int slice, int G) {
+__host__ __device__ inline Layout make_layout(int nrep, int slice, int G, int rtab_words) {
     Layout L;
     int o = 0;
     L.bad = o;  o += 16;
@@ -74,6 +77,10 @@ __host__ __device__ inline Layout make_layout(int nrep, int slice, int G) {
     L.wsum = o; o = al16(o + 32 * 4);
     L.hw = o;   o = al16(o + kWarps * nrep * 4);
     L.pk = o;   o = al16(o + slice * 4);
+    L.rtab = o; o = al16(o + rtab_words * 4);
+    L.base = o; o = al16(o + nrep * 4);
+    L.se = o;   o = al16(o + slice * 4);
+    L.sg = o;   o = al16(o + slice * 4);
     L.total = o;
     return L;
 }
@@ -121,7 +128,7 @@ __device__ void block_exscan(const int32_t *v, int32_t *out, int n, int32_t *wsu
 __global__ void __launch_bounds__(kThreads, 1) layout_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t R = cluster_nctarank(), cta = cluster_ctarank();
-    const Layout L = make_layout(p.nrep, p.slice, p.G);
+    const Layout L = make_layout(p.nrep, p.slice, p.G, p.rtab_smem ? p.N * p.G : 0);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nrep = p.nrep;
     unsigned long long *s_bad = reinterpret_cast<unsigned long long *>(smem + L.bad);
@@ -133,14 +140,40 @@ __global__ void __launch_bounds__(kThreads, 1) layout_kernel(const Params p) {
     int32_t *s_wsum = reinterpret_cast<int32_t *>(smem + L.wsum);
     int32_t *s_hw = reinterpret_cast<int32_t *>(smem + L.hw);
     uint32_t *s_pk = reinterpret_cast<uint32_t *>(smem + L.pk);
+    int32_t *s_rtab = reinterpret_cast<int32_t *>(smem + L.rtab);
+    int32_t *s_base = reinterpret_cast<int32_t *>(smem + L.base);
+    int32_t *s_e = reinterpret_cast<int32_t *>(smem + L.se);
+    int32_t *s_g = reinterpret_cast<int32_t *>(smem + L.sg);
 
     const int64_t beg = static_cast<int64_t>(cta) * p.slice;
     const int64_t rem = p.num_pairs - beg;
     const int n_local = rem <= 0 ? 0 : static_cast<int>(rem < p.slice ? rem : p.slice);
+    // PDL: shared-memory prologue, then wait for the routing kernel's outputs
+    griddep_launch_dependents();
     if (tid == 0) *s_bad = kNoBad;
     for (int i = tid; i < kWarps * nrep; i += kThreads) s_hw[i] = 0;
+    griddep_wait();
     for (int i = tid; i <= p.G; i += kThreads) s_sb[i] = __ldg(p.slot_base + i);
+    if (p.rtab_smem)  // the replica table (N * G words) once into shared memory: the
+        for (int i = tid; i < p.N * p.G; i += kThreads) s_rtab[i] = __ldg(p.rid_tab + i);  // lookups are LDS
+    // the CTA's pairs (expert, serving rank) into shared memory with independent
+    // 16-byte loads, all in flight at once: the rank loop below then never waits
+    // on global memory
+    {
+        const int32_t *ge = p.ids + beg, *gg = p.pair_rank + beg;
+        const bool vec = ((reinterpret_cast<uintptr_t>(ge) | reinterpret_cast<uintptr_t>(gg)) & 15) == 0;
+        const int n4 = vec ? (n_local >> 2) : 0;
+        for (int i = tid; i < n4; i += kThreads) {
+            reinterpret_cast<int4 *>(s_e)[i] = __ldg(reinterpret_cast<const int4 *>(ge) + i);
+            reinterpret_cast<int4 *>(s_g)[i] = __ldg(reinterpret_cast<const int4 *>(gg) + i);
+        }
+        for (int i = 4 * n4 + tid; i < n_local; i += kThreads) {
+            s_e[i] = __ldg(ge + i);
+            s_g[i] = __ldg(gg + i);
+        }
+    }
     __syncthreads();
+    const int32_t *rtab = p.rtab_smem ? s_rtab : p.rid_tab;
 
     // (1) warp sub-slices, match_any ranks
     const int ws = (((n_local + kWarps - 1) / kWarps) + 31) & ~31;
@@ -151,13 +184,13 @@ __global__ void __launch_bounds__(kThreads, 1) layout_kernel(const Params p) {
         const int i = p0 + lane;
         int rid = -1;
         if (i < we) {
-            const int e = __ldg(p.ids + beg + i);
-            const int g = __ldg(p.pair_rank + beg + i);
+            const int e = s_e[i];
+            const int g = s_g[i];
             const unsigned long long gi = static_cast<unsigned long long>(beg + i);
             if (static_cast<unsigned>(e) >= static_cast<unsigned>(p.N)) {
                 my_bad = min(my_bad, gi << 1);
             } else if (static_cast<unsigned>(g) >= static_cast<unsigned>(p.G) ||
-                       (rid = __ldg(p.rid_tab + static_cast<int64_t>(e) * p.G + g)) < 0) {
+                       (rid = rtab[static_cast<int64_t>(e) * p.G + g]) < 0) {
                 rid = -1;
                 my_bad = min(my_bad, (gi << 1) | 1ull);
             }
@@ -200,11 +233,17 @@ __global__ void __launch_bounds__(kThreads, 1) layout_kernel(const Params p) {
             bad = min(bad, (static_cast<unsigned long long>(hi) << 32) | lo);
         }
         for (int rid = tid; rid < nrep; rid += kThreads) {
-            int32_t pre = 0, all = 0;
-            for (uint32_t q = 0; q < R; ++q) {
-                const int32_t v = (q == cta) ? s_tot[rid] : static_cast<int32_t>(dsmem_ld(s_tot + rid, q));
-                pre += (q < cta) ? v : 0;
-                all += v;
+            // every peer's load in flight before the first use (R <= 16)
+            int32_t v[kMaxCluster];
+#pragma unroll
+            for (int q = 0; q < kMaxCluster; ++q)
+                v[q] = (q < static_cast<int>(R) && q != static_cast<int>(cta))
+                           ? static_cast<int32_t>(dsmem_ld(s_tot + rid, q)) : 0;
+            int32_t pre = 0, all = s_tot[rid];
+#pragma unroll
+            for (int q = 0; q < kMaxCluster; ++q) {
+                pre += (q < static_cast<int>(cta)) ? v[q] : 0;
+                all += v[q];
             }
             s_pre[rid] = pre;
             s_loc[rid] = all;  // global totals (scanned below)
@@ -234,8 +273,11 @@ __global__ void __launch_bounds__(kThreads, 1) layout_kernel(const Params p) {
     block_exscan(s_loc, s_off, nrep, s_wsum);
     if (cta == 0)
         for (int i = tid; i <= nrep; i += kThreads) p.rep_off[i] = s_off[i];
-    // per replica: global offset + this CTA's prefix (s_loc reused)
-    for (int rid = tid; rid < nrep; rid += kThreads) s_loc[rid] = s_off[rid] + s_pre[rid];
+    // per replica: global offset + this CTA's prefix - the first row of its rank
+    // (replicas are numbered rank-major: rank g owns [sb[g], sb[g + 1]))
+    for (int g = 0; g < p.G; ++g)
+        for (int rid = s_sb[g] + tid; rid < s_sb[g + 1]; rid += kThreads)
+            s_base[rid] = s_off[rid] + s_pre[rid] - s_off[s_sb[g]];
     __syncthreads();
 
     // (4) rows, relative to the first row of the serving rank
@@ -243,9 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1) layout_kernel(const Params p) {
         const uint32_t pk = s_pk[i];
         const int rid = static_cast<int>(pk >> 16);
         const int w = i / ws;
-        const int g = __ldg(p.pair_rank + beg + i);
-        p.pair_row[beg + i] =
-            s_loc[rid] - s_off[s_sb[g]] + s_hw[w * nrep + rid] + static_cast<int>(pk & 0xffffu);
+        p.pair_row[beg + i] = s_base[rid] + s_hw[w * nrep + rid] + static_cast<int>(pk & 0xffffu);
     }
     if (cta == 0 && tid == 0) {
         p.status[0] = METRO_OK;
@@ -314,26 +354,34 @@ int metro_dispatch_layout_v1(const int32_t *ids, const int32_t *pair_rank, int64
     const int64_t slice64 = (num_pairs + R - 1) / R;
     if (slice64 > kMaxSlice) return METRO_EDIMS;
     const int slice = static_cast<int>(slice64 < 32 ? 32 : slice64);
-    const Layout L = make_layout(nrep, slice, G);
+    // stage the replica table in shared memory when it fits (N * G words)
+    int rtab_smem = 1;
+    Layout L = make_layout(nrep, slice, G, N * G);
+    if (L.total > 232448) {
+        rtab_smem = 0;
+        L = make_layout(nrep, slice, G, 0);
+    }
     if (L.total > 232448) return METRO_EDIMS;
     cudaError_t e = prepare_layout();
     if (e != cudaSuccess) return metro::cuda_fail(e);
     Params p;
     p.ids = ids; p.pair_rank = pair_rank; p.num_pairs = num_pairs; p.slice = slice;
     p.rid_tab = rid_tab; p.slot_base = slot_base; p.N = N; p.G = G; p.nrep = nrep;
-    p.pair_row = pair_row; p.rep_off = rep_off; p.status = status;
+    p.pair_row = pair_row; p.rep_off = rep_off; p.status = status; p.rtab_smem = rtab_smem;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(R, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = L.total;
     cfg.stream = static_cast<cudaStream_t>(stream);
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = R;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // griddep_wait before global reads
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     e = cudaLaunchKernelEx(&cfg, layout_kernel, p);
     if (e != cudaSuccess) return metro::cuda_fail(e);
     return METRO_OK;
