@@ -130,7 +130,7 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
 template <int W>
 __global__ void __launch_bounds__(kServeThreads, 1)
     metro_serve_kernel(const Params base, ServeCtl *ctl, uint32_t seq, uint64_t idle_ns, int fence_mode,
-                       uint32_t stagger) {
+                       uint32_t stagger, int32_t *scratch) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31;
     const Layout L = make_layout(kMetroIds, base.N, W, 1, base.slice, base.C, base.staged);
@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(kServeThreads, 1)
                     const int i = i0 + u * kThreads;
                     if (i < n4) {
                         if (staged) reinterpret_cast<int4 *>(s_ids)[i] = v[u];
+                        else reinterpret_cast<int4 *>(scratch)[i] = v[u];  // HBM copy for the second pass
                         const int ev[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
@@ -276,6 +277,7 @@ __global__ void __launch_bounds__(kServeThreads, 1)
             for (int i = n4 * 4 + tid; i < n; i += kThreads) {
                 const int e = ld_relaxed_sys_s32(p.ids + i);
                 if (staged) s_ids[i] = e;
+                else scratch[i] = e;
                 if (static_cast<unsigned>(e) < static_cast<unsigned>(p.N))
                     atomicAdd(&s_hist[e * p.C + (lane & cm)], 1);
                 else
@@ -298,12 +300,13 @@ __global__ void __launch_bounds__(kServeThreads, 1)
                 const int n4 = n >> 2;
                 const int4 *src4 = reinterpret_cast<const int4 *>(p.ids);
                 for (int i = tid; i < n4; i += kThreads) {
-                    const int4 v = staged ? reinterpret_cast<const int4 *>(s_ids)[i] : ld_relaxed_sys_v4(src4 + i);
+                    const int4 v = staged ? reinterpret_cast<const int4 *>(s_ids)[i]
+                                          : reinterpret_cast<const int4 *>(scratch)[i];
                     reinterpret_cast<int4 *>(p.pair_rank)[i] =
                         make_int4(s_choice[v.x], s_choice[v.y], s_choice[v.z], s_choice[v.w]);
                 }
                 for (int i = n4 * 4 + tid; i < n; i += kThreads)
-                    p.pair_rank[i] = s_choice[staged ? s_ids[i] : ld_relaxed_sys_s32(p.ids + i)];
+                    p.pair_rank[i] = s_choice[staged ? s_ids[i] : scratch[i]];
             }
             for (int e = tid; e < p.N; e += kThreads) p.choice[e] = s_choice[e];
             if (tid == 0) {
@@ -346,7 +349,8 @@ static int serve_plan(int N, int W, int64_t max_pairs, Params &p) {
     int C0 = 32;
     while (C0 > 1 && N * C0 * 4 > 64 * 1024) C0 >>= 1;
     // staged: the whole batch in shared memory; otherwise (batches beyond ~40k
-    // pairs) the ids are read from host memory a second time for the pair ranks
+    // pairs) the first pass also copies the ids to a device scratch buffer that
+    // the pair-rank pass reads (HBM instead of a second PCIe read)
     for (int staged = 1; staged >= 0; --staged)
         for (int C = C0; C >= 1; C >>= 1) {
             const Layout L = make_layout(kMetroIds, N, W, 1, slice, C, staged);
@@ -374,6 +378,7 @@ struct metro_server {
     uint64_t idle_ns = 0;
     uint32_t seq = 0;
     int fence_mode = 0, doorbell_warps = 2;
+    int32_t *scratch = nullptr;  // unstaged mode: device copy of the ids
     uint32_t stagger = 1000;
     bool sent_ptrs = false;
     int64_t max_pairs = 0, launches = 0;
@@ -399,10 +404,10 @@ static int serve_launch(metro_server *s) {
     __atomic_store_n(&s->ctl->state, kServeLaunched, __ATOMIC_RELEASE);
     const uint32_t seq0 = s->seq;  // the last request this server completed
     switch (s->W) {
-        case 1: metro_serve_kernel<1><<<1, kThreads + 32 * s->doorbell_warps, s->smem, s->stream>>>(s->base, s->ctl, seq0, s->idle_ns, s->fence_mode, s->stagger); break;
-        case 2: metro_serve_kernel<2><<<1, kThreads + 32 * s->doorbell_warps, s->smem, s->stream>>>(s->base, s->ctl, seq0, s->idle_ns, s->fence_mode, s->stagger); break;
-        case 3: metro_serve_kernel<3><<<1, kThreads + 32 * s->doorbell_warps, s->smem, s->stream>>>(s->base, s->ctl, seq0, s->idle_ns, s->fence_mode, s->stagger); break;
-        case 4: metro_serve_kernel<4><<<1, kThreads + 32 * s->doorbell_warps, s->smem, s->stream>>>(s->base, s->ctl, seq0, s->idle_ns, s->fence_mode, s->stagger); break;
+        case 1: metro_serve_kernel<1><<<1, kThreads + 32 * s->doorbell_warps, s->smem, s->stream>>>(s->base, s->ctl, seq0, s->idle_ns, s->fence_mode, s->stagger, s->scratch); break;
+        case 2: metro_serve_kernel<2><<<1, kThreads + 32 * s->doorbell_warps, s->smem, s->stream>>>(s->base, s->ctl, seq0, s->idle_ns, s->fence_mode, s->stagger, s->scratch); break;
+        case 3: metro_serve_kernel<3><<<1, kThreads + 32 * s->doorbell_warps, s->smem, s->stream>>>(s->base, s->ctl, seq0, s->idle_ns, s->fence_mode, s->stagger, s->scratch); break;
+        case 4: metro_serve_kernel<4><<<1, kThreads + 32 * s->doorbell_warps, s->smem, s->stream>>>(s->base, s->ctl, seq0, s->idle_ns, s->fence_mode, s->stagger, s->scratch); break;
         default: return METRO_EDIMS;
     }
     e = cudaGetLastError();
@@ -458,6 +463,10 @@ int metro_server_create_v1(const uint32_t *mask, int32_t N, int32_t G, int64_t m
         else memset(s->ctl, 0, sizeof(ServeCtl));
     }
     if (rc == METRO_OK && !host_mapped(s->ctl)) rc = METRO_EARG;  // UVA identity mapping required
+    if (rc == METRO_OK && !s->base.staged) {
+        e = cudaMalloc(reinterpret_cast<void **>(&s->scratch), static_cast<size_t>(s->base.slice) * 4);
+        if (e != cudaSuccess) rc = cuda_fail(e);
+    }
     if (rc == METRO_OK) {
         // non-blocking: the resident CTA never serialises the legacy default stream
         e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
@@ -560,6 +569,7 @@ int metro_server_destroy_v1(metro_server *s) {
         cudaFreeHost(s->ctl);
     }
     if (s->stream) cudaStreamDestroy(s->stream);
+    if (s->scratch) cudaFree(s->scratch);
     delete s;
     return rc;
 }
