@@ -404,8 +404,13 @@ int metro_exchange_alloc(size_t bytes, void **dev_ptr_out) {
     void *p = nullptr;
     cudaError_t e = cudaMalloc(&p, bytes);  // its own allocation: an IPC handle maps exactly it
     if (e != cudaSuccess) return cuda_fail(e);
-    e = cudaMemset(p, 0, bytes);
-    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    // zeroed on a private stream (no device-wide synchronise: a resident router
+    // CTA elsewhere in the process would hold it up)
+    cudaStream_t zs = nullptr;
+    e = cudaStreamCreateWithFlags(&zs, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p, 0, bytes, zs);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(zs);
+    if (zs) cudaStreamDestroy(zs);
     if (e != cudaSuccess) {
         cudaFree(p);
         return cuda_fail(e);
