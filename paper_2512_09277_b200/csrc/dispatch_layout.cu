@@ -149,10 +149,10 @@ __global__ void __launch_bounds__(kThreads, 1) layout_kernel(const Params p) {
     const int64_t rem = p.num_pairs - beg;
     const int n_local = rem <= 0 ? 0 : static_cast<int>(rem < p.slice ? rem : p.slice);
     // PDL: shared-memory prologue, then wait for the routing kernel's outputs
-    griddep_launch_dependents();
     if (tid == 0) *s_bad = kNoBad;
     for (int i = tid; i < kWarps * nrep; i += kThreads) s_hw[i] = 0;
     griddep_wait();
+    griddep_launch_dependents();  // only once this kernel runs: at most one dependent waits
     for (int i = tid; i <= p.G; i += kThreads) s_sb[i] = __ldg(p.slot_base + i);
     if (p.rtab_smem)  // the replica table (N * G words) once into shared memory: the
         for (int i = tid; i < p.N * p.G; i += kThreads) s_rtab[i] = __ldg(p.rid_tab + i);  // lookups are LDS

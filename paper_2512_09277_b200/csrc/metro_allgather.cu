@@ -94,10 +94,14 @@ __global__ void __launch_bounds__(kThreads, 1) metro_allgather_kernel(const XPar
     xstamp(x, 0);
     // ---- stage + count the local ids (metro_ids_kernel's phases A-B, one CTA)
     const StagePlan sp = stage_plan<W>(p, 0, n_local, true);
-    if (tid == 0) stage_issue(p, L, smem, 0, sp);
+    // PDL: shared-memory prologue while the previous kernel finishes; no global
+    // (or peer) access before griddep_wait
     int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
     init_misc(misc);
     zero_smem(smem, L.aux, L.part);
+    griddep_wait();
+    griddep_launch_dependents();  // only once this kernel runs: at most one dependent waits
+    if (tid == 0) stage_issue(p, L, smem, 0, sp);
     stage_rest(p, L, smem, 0, n_local, true, sp);
     // (the threads that initialised these misc words: program order, no race)
     if (tid == X_EPOCH) misc[X_EPOCH] = static_cast<int32_t>(*reinterpret_cast<volatile uint32_t *>(own) + 1u);
@@ -312,8 +316,17 @@ static int x_launch(const XParams &x, int smem, cudaStream_t s) {
         if (e != cudaSuccess) return cuda_fail(e);
         done[dev] = true;
     }
-    metro_allgather_kernel<W><<<1, kThreads, smem, s>>>(x);
-    cudaError_t e = cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // griddep_wait before global access
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, metro_allgather_kernel<W>, x);
     return e == cudaSuccess ? METRO_OK : cuda_fail(e);
 }
 

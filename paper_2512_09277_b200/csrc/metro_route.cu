@@ -56,11 +56,11 @@ __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) 
     const StagePlan sp = stage_plan<W>(p, beg, n_local, !GATE && p.staged != 0);
     // PDL: shared-memory prologue while the previous kernel in the stream finishes;
     // no global access before griddep_wait (the ids are that kernel's output)
-    griddep_launch_dependents();
     int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
     init_misc(misc);
     zero_smem(smem, L.aux, L.part);  // forced counts + histogram
     griddep_wait();
+    griddep_launch_dependents();  // only once this kernel runs: at most one dependent waits
     if (threadIdx.x == 0) stage_issue(p, L, smem, beg, sp);
     if (R > 1) cluster_arrive_release();  // after thread 0 initialised the mbarriers
     stamp(p, 0);
@@ -156,8 +156,8 @@ __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) 
 // workspace for the next launch.
 template <int W, int NPL>
 __global__ void __launch_bounds__(kThreads, 1) metro_gate_kernel(const Params p) {
-    griddep_launch_dependents();
     griddep_wait();  // PDL launch: no global access before the previous kernel completes
+    griddep_launch_dependents();  // only once this kernel runs: at most one dependent waits
     extern __shared__ __align__(128) unsigned char smem[];
     const Layout L = make_layout(kMetroLoads, p.N, W, 1, 0, 1, 0);
     const int tid = threadIdx.x, N = p.N, k = p.top_k;
@@ -239,8 +239,8 @@ __global__ void __launch_bounds__(kThreads, 1) metro_gate_kernel(const Params p)
 // METRO from loads (compat route_metro(T, A)) or from a caller order (metro-parallel).
 template <int W>
 __global__ void __launch_bounds__(kThreads, 1) metro_loads_kernel(const Params p, int ordered) {
-    griddep_launch_dependents();
     griddep_wait();  // PDL launch: no global access before the previous kernel completes
+    griddep_launch_dependents();  // only once this kernel runs: at most one dependent waits
     extern __shared__ __align__(128) unsigned char smem[];
     const Layout L = make_layout(ordered ? kMetroOrdered : kMetroLoads, p.N, W, 1, 0, 1, 0);
     const StagePlan sp = stage_plan<W>(p, 0, 0, false);
@@ -360,8 +360,8 @@ __device__ bool eplb_counts_and_x(const Params &p, const Layout &L, unsigned cha
 
 template <int W, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) eplb_ids_kernel(const Params p) {
-    griddep_launch_dependents();
     griddep_wait();  // PDL launch: no global access before the previous kernel completes
+    griddep_launch_dependents();  // only once this kernel runs: at most one dependent waits
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t R = cluster_nctarank(), rank = cluster_ctarank();
     const Layout L = make_layout(kEplbIds, p.N, W, R, p.slice, p.C, p.staged, PAIR);
@@ -449,8 +449,8 @@ __global__ void __launch_bounds__(kThreads, 1) eplb_ids_kernel(const Params p) {
 
 template <int W>
 __global__ void __launch_bounds__(kThreads, 1) eplb_loads_kernel(const Params p) {
-    griddep_launch_dependents();
     griddep_wait();  // PDL launch: no global access before the previous kernel completes
+    griddep_launch_dependents();  // only once this kernel runs: at most one dependent waits
     extern __shared__ __align__(128) unsigned char smem[];
     const Layout L = make_layout(kEplbLoads, p.N, W, 1, 0, 1, 0);
     const StagePlan sp = stage_plan<W>(p, 0, 0, false);

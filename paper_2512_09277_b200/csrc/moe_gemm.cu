@@ -148,6 +148,12 @@ __device__ __forceinline__ int map_index(int n) {  // smallest box height >= n
     return i;
 }
 
+// PDL (programmatic dependent launch): every kernel here signals its dependents
+// first and waits (griddepcontrol.wait) for its predecessors before the first
+// global access that may depend on them.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 template <typename TL>
 __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_constant__ Maps maps, const Params p) {
     constexpr int STAGES = TL::kStages, B_BYTES = TL::kBBytes, MAXN_T = TL::kN, TMEM_COLS = TL::kTmemCols;
@@ -162,6 +168,10 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int kblocks = p.K / BK;
+    if (warp == 4 && lane == 0)  // the tensor map is a kernel parameter: prefetch before the wait
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.w)) : "memory");
+    pdl_wait();
+    pdl_launch_dependents();  // only once this kernel runs: at most one dependent waits
     const int n_items = p.n_items_dev ? min(p.n_items, *p.n_items_dev) : p.n_items;
 
     if (warp == 4 && lane == 0) {
@@ -174,7 +184,6 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.w)) : "memory");
     }
     if (warp == 5) {  // TMEM allocation by one full warp
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -278,6 +287,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
 // H[t, i] = silu(GU[t, i]) * GU[t, I + i]   (gate | up halves of the first projection)
 __global__ void silu_mul_kernel(const __nv_bfloat16 *__restrict__ gu, int T, int I, __nv_bfloat16 *__restrict__ h,
                                 const int32_t *rows_dev) {
+    pdl_wait();
+    pdl_launch_dependents();  // only once this kernel runs: at most one dependent waits
     if (rows_dev) T = min(T, *rows_dev);
     const int64_t total = static_cast<int64_t>(T) * I;
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -301,6 +312,8 @@ __global__ void __launch_bounds__(kItThreads) layout_items_kernel(const int32_t 
                                                                   int cap1, int cap2, int32_t *counts) {
     __shared__ int32_t s_w[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    pdl_wait();
+    pdl_launch_dependents();  // only once this kernel runs: at most one dependent waits
     const int b0 = slot_base[rank], S = slot_base[rank + 1] - b0;
     const int base_row = rep_off[b0];
     int run = 0;  // chunks of the slots already done
@@ -355,6 +368,8 @@ __global__ void __launch_bounds__(kItThreads) layout_items_kernel(const int32_t 
 __global__ void gather_rows_kernel(const uint4 *__restrict__ src, int row_vecs, int k,
                                    const int32_t *__restrict__ pair_rank, const int32_t *__restrict__ pair_row,
                                    int64_t num_pairs, int rank, uint4 *__restrict__ dst, int rows_cap) {
+    pdl_wait();
+    pdl_launch_dependents();  // only once this kernel runs: at most one dependent waits
     const int64_t warp_id = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -370,6 +385,23 @@ __global__ void gather_rows_kernel(const uint4 *__restrict__ src, int row_vecs, 
 
 // ---------------------------------------------------------------- host
 static thread_local int g_err = 0;
+
+// launch with programmatic stream serialisation (every kernel above waits with
+// griddepcontrol.wait before touching its predecessors' outputs)
+template <typename K, typename... Args>
+static cudaError_t launch_pdl(K kernel, int grid, int block, int smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(block, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -439,11 +471,9 @@ static int launch_gemm(const void *W, int32_t E, int32_t M, int32_t K, const voi
     prm.Y = static_cast<__nv_bfloat16 *>(Y);
     prm.ldy = M;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (max_item_tokens <= NarrowTile::kN)
-        moe_gemm_kernel<NarrowTile><<<grid, kThreads, NarrowTile::kSmem, s>>>(maps, prm);
-    else
-        moe_gemm_kernel<WideTile><<<grid, kThreads, WideTile::kSmem, s>>>(maps, prm);
-    const cudaError_t e = cudaGetLastError();
+    const cudaError_t e = max_item_tokens <= NarrowTile::kN
+                              ? launch_pdl(moe_gemm_kernel<NarrowTile>, grid, kThreads, NarrowTile::kSmem, s, maps, prm)
+                              : launch_pdl(moe_gemm_kernel<WideTile>, grid, kThreads, WideTile::kSmem, s, maps, prm);
     if (e != cudaSuccess) {
         g_err = e;
         return METRO_ECUDA;
@@ -493,10 +523,11 @@ METRO_API int moe_layout_items_v1(const int32_t *rep_off, const int32_t *slot_ba
         (M2 > 0 && !items2))
         return METRO_EARG;
     if (M1 % BM || (M2 > 0 && M2 % BM)) return METRO_EDIMS;
-    layout_items_kernel<<<1, kItThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-        rep_off, slot_base, rank, M1 / BM, M2 > 0 ? M2 / BM : 0, reinterpret_cast<Item *>(items1),
-        reinterpret_cast<Item *>(items2), cap1, cap2, counts);
-    const cudaError_t e = cudaGetLastError();
+    const cudaError_t e = launch_pdl(layout_items_kernel, 1, kItThreads, 0, static_cast<cudaStream_t>(stream),
+                                     rep_off, slot_base, static_cast<int>(rank), static_cast<int>(M1 / BM),
+                                     static_cast<int>(M2 > 0 ? M2 / BM : 0), reinterpret_cast<Item *>(items1),
+                                     reinterpret_cast<Item *>(items2), static_cast<int>(cap1),
+                                     static_cast<int>(cap2), counts);
     if (e != cudaSuccess) {
         g_err = e;
         return METRO_ECUDA;
@@ -515,10 +546,10 @@ METRO_API int moe_gather_rows_v1(const void *src, int32_t row_bytes, int32_t top
     if (num_pairs == 0) return METRO_OK;
     const int64_t blocks = (num_pairs + 7) / 8;
     const int grid = static_cast<int>(blocks < 148 * 16 ? blocks : 148 * 16);
-    gather_rows_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<const uint4 *>(src), row_bytes / 16, top_k, pair_rank, pair_row, num_pairs, rank,
-        static_cast<uint4 *>(dst), rows_cap);
-    const cudaError_t e = cudaGetLastError();
+    const cudaError_t e = launch_pdl(gather_rows_kernel, grid, 256, 0, static_cast<cudaStream_t>(stream),
+                                     static_cast<const uint4 *>(src), static_cast<int>(row_bytes / 16),
+                                     static_cast<int>(top_k), pair_rank, pair_row, num_pairs,
+                                     static_cast<int>(rank), static_cast<uint4 *>(dst), static_cast<int>(rows_cap));
     if (e != cudaSuccess) {
         g_err = e;
         return METRO_ECUDA;
@@ -543,9 +574,9 @@ static int launch_silu(const void *GU, int32_t T, int32_t I, void *H, const int3
     if (T == 0) return METRO_OK;
     const int64_t total = static_cast<int64_t>(T) * I;
     const int grid = static_cast<int>(total / 256 + 1 < 148 * 8 ? total / 256 + 1 : 148 * 8);
-    silu_mul_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<const __nv_bfloat16 *>(GU), T, I, static_cast<__nv_bfloat16 *>(H), rows_dev);
-    const cudaError_t e = cudaGetLastError();
+    const cudaError_t e = launch_pdl(silu_mul_kernel, grid, 256, 0, static_cast<cudaStream_t>(stream),
+                                     static_cast<const __nv_bfloat16 *>(GU), static_cast<int>(T),
+                                     static_cast<int>(I), static_cast<__nv_bfloat16 *>(H), rows_dev);
     if (e != cudaSuccess) {
         g_err = e;
         return METRO_ECUDA;
