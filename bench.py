@@ -48,6 +48,13 @@ CONFIGS = {
 for _b in (64, 128, 256, 512, 2048, 4096, 8192):
     CONFIGS[f"ds_b{_b}"] = dict(workload=f"DeepSeek-V3 shape, decode batch {_b}", N=256, k=8, G=8,
                                 ratio=1.5, B=_b)
+# Zipf skew of the decode batch's expert popularity (BASELINE configs[2]; the
+# placement is always built from a Zipf(1.2) history, as the reference's fixtures)
+for _s in (0.5, 2.0):
+    for _b in (64, 1024, 8192):
+        CONFIGS[f"ds_b{_b}_skew{_s}"] = dict(workload=f"DeepSeek-V3 shape, decode batch {_b}, Zipf({_s}) "
+                                                     f"expert popularity", N=256, k=8, G=8, ratio=1.5, B=_b,
+                                             skew=_s)
 
 POOL = 32          # distinct batches resident in HBM, cycled through the steps
 FLUSH_BYTES = 256 << 20
@@ -75,7 +82,7 @@ def workload(cfg, world: int):
     from paper_2512_09277_b200.placement import gen_zipf_topk, make_placement
 
     A = make_placement(cfg["N"], cfg["G"], cfg["ratio"], POP_SEED).matrix
-    batches = [gen_zipf_topk(cfg["N"], cfg["k"], cfg["B"], SKEW, 1000 + s, popularity_seed=POP_SEED)
+    batches = [gen_zipf_topk(cfg["N"], cfg["k"], cfg["B"], cfg.get("skew", SKEW), 1000 + s, popularity_seed=POP_SEED)
                for s in range(POOL)]
     return A, batches
 
@@ -228,7 +235,7 @@ def run_reference(args, cfg, rank: int, world: int):
     return {
         "impl": "reference", "metric": METRIC, "value": us, "unit": "us/layer", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
-        "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": data_str(),
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": data_str(cfg),
         "config": dict(config_dict(args, cfg, world), l2="n/a (host CPU path)",
                        parallelism="single host thread, one layer per step"),
         "cpu_baseline": {"value": us, "unit": "us/layer", "cores": 1, "kind": "port", "sample": sample,
@@ -237,9 +244,10 @@ def run_reference(args, cfg, rank: int, world: int):
     }
 
 
-def data_str():
-    return ("synthetic: Zipf(1.2) expert popularity, top-8 distinct ids per token by Gumbel top-k; "
-            "EPLB placement from a Zipf history (reference generators, popularity seed 7)")
+def data_str(cfg=None):
+    skew = (cfg or {}).get("skew", SKEW)
+    return (f"synthetic: Zipf({skew}) expert popularity, top-8 distinct ids per token by Gumbel top-k; "
+            "EPLB placement from a Zipf(1.2) history (reference generators, popularity seed 7)")
 
 
 def config_dict(args, cfg, world):
@@ -495,7 +503,9 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
                      "launch_per_call_us": statistics.mean(per1) * 1e6,
                      "launch_per_call_api": "HostRouter.run (metro_route_host_v1, zero-copy, one launch + sync)"}
     else:
-        dr = DistributedRouter(pl, lt, k, "metro", args.cluster)
+        use_fused = method.get("fused_exchange_route_us") is not None
+        dr = None if use_fused else DistributedRouter(pl, lt, k, "metro", args.cluster)
+        local_d = torch.empty((lt, k), dtype=torch.int32, device=dev)
         hosts = [torch.from_numpy(b[rank * lt:(rank + 1) * lt].copy()).pin_memory() for b in batches]
         small_h = torch.empty(8 + cfg["G"] + cfg["N"], dtype=torch.int32).pin_memory()
         own_h = torch.empty(lt * k, dtype=torch.int32).pin_memory()
@@ -505,19 +515,26 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
             flush.zero_()
             sync_all()
             t0 = time.perf_counter()
-            dr.local.copy_(hosts[i % POOL].view(lt, k), non_blocking=True)
-            o = dr.step()
+            if use_fused:  # the product path: fused exchange + route (metro_exchange.h)
+                local_d.copy_(hosts[i % POOL].view(lt, k), non_blocking=True)
+                o = fz.step(local_d)
+                own = o.pair_rank
+            else:
+                dr.local.copy_(hosts[i % POOL].view(lt, k), non_blocking=True)
+                o = dr.step()
+                own = dr.own_pair_rank()
             small_d[0:4].copy_(o.status)
             small_d[4:5].copy_(o.lam)
             small_d[8:8 + cfg["G"]].copy_(o.rank_counts)
             small_d[8 + cfg["G"]:].copy_(o.choice)
             small_h.copy_(small_d, non_blocking=True)
-            own_h.copy_(dr.own_pair_rank(), non_blocking=True)
+            own_h.copy_(own, non_blocking=True)
             torch.cuda.current_stream().synchronize()
             if i >= 10:
                 per.append(time.perf_counter() - t0)
         e2e_us = max_over_ranks([statistics.mean(per)])[0] * 1e6
-        e2e_extra = {"api": "DistributedRouter (NCCL all-gather + route) from pinned host buffers"}
+        e2e_extra = {"api": ("FusedAllGatherRouter.step (fused exchange + route)" if use_fused else
+                             "DistributedRouter (NCCL all-gather + route)") + " from pinned host buffers"}
         h2d = lt * k * 4
         d2h = small_h.numel() * 4 + lt * k * 4
 
@@ -530,7 +547,7 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
     res = {
         "metric": METRIC, "value": step_ms * 1e3, "unit": "us/layer", "n_gpus": world, "steps": K_eff,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "int32", "data": data_str(),
+        "vs_baseline": None, "dtype": "int32", "data": data_str(cfg),
         "config": config_dict(args, cfg, world),
         "e2e": dict({"value": e2e_us, "unit": "us/layer", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                     **e2e_extra),
