@@ -591,6 +591,16 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
             "roofline": {"bound": "hbm", "achieved": m["metro"]["achieved_gbs"], "peak": m["peak_gbs"],
                          "unit": "GB/s", "frac": m["metro"]["frac"], "kernel": "moe_gemm_kernel"},
         }
+        # the same with FP8 (E4M3) experts, as DeepSeek-V3 ships them: half the bytes
+        m8 = moe_layer_bench.run(batches=2, reps=3, B=cfg["B"], ratio=cfg["ratio"], dtype="fp8")
+        res["moe_layer_k3_fp8"] = {
+            "what": "as moe_layer_k3 with E4M3 expert weights (scale per 128-row block) and E4M3 activations "
+                    "(scale per token), tcgen05 kind::f8f6f4",
+            "metro": m8["metro"], "eplb": m8["eplb"],
+            "ffn_speedup_metro_vs_eplb": m8["ffn_speedup_metro_vs_eplb"],
+            "device_layer_speedup_metro_vs_eplb": m8["device_layer_speedup_metro_vs_eplb"],
+            "routing_share_of_metro_layer": step_ms * 1e3 / m8["metro"]["device_layer_us"],
+        }
     if world == 1:
         us, layers, outs = cpu_route_layers(A, batches, args.cpu_seconds)
         parity = all(int(o[3][0]) == lm for o, lm in zip(outs, lam_m))

@@ -18,6 +18,7 @@
 // Weights are streamed exactly once per item; the kernel is HBM-bound.
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp8.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <stdint.h>
@@ -57,6 +58,9 @@ struct Item {
 };
 
 struct Params {
+    const float *w_scale;  // FP8: per (expert slot, 128-row block) dequantisation scale [E][M / 128]
+    const float *x_scale;  // FP8: per token row [T]
+    int mblocks;           // M / 128
     const Item *items;
     int n_items;                // capacity when n_items_dev is set
     const int32_t *n_items_dev; // nullable: item count produced on device (moe_layout_items_v1)
@@ -124,6 +128,19 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t 
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
 }
+// FP8 (E4M3 A and B, f32 accumulate): same descriptors, K = 32 elements per MMA
+// (32 bytes, as bf16's K = 16), a/b format fields 0 = E4M3
+__device__ __forceinline__ uint32_t idesc_e4m3(int n) {
+    return (1u << 4) | (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
+}
+__device__ __forceinline__ void umma_e4m3(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint64_t *b) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
                  : "memory");
@@ -154,9 +171,13 @@ __device__ __forceinline__ int map_index(int n) {  // smallest box height >= n
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-template <typename TL>
+// FP8: a 128-byte swizzled row holds 128 E4M3 elements (64 bf16), so one k-block
+// is 128 elements; the shared-memory bytes per stage and the descriptors are the
+// same as bf16's.
+template <typename TL, bool FP8 = false>
 __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_constant__ Maps maps, const Params p) {
     constexpr int STAGES = TL::kStages, B_BYTES = TL::kBBytes, MAXN_T = TL::kN, TMEM_COLS = TL::kTmemCols;
+    constexpr int BKE = FP8 ? 2 * BK : BK;  // elements per k-block
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char *sA = smem;
@@ -167,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     uint64_t *tempty = tfull + 2;       // [2]
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int kblocks = p.K / BK;
+    const int kblocks = p.K / BKE;
     if (warp == 4 && lane == 0)  // the tensor map is a kernel parameter: prefetch before the wait
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.w)) : "memory");
     pdl_wait();
@@ -208,8 +229,8 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], A_BYTES + bbytes);
-                    tma_load_3d(sA + stage * A_BYTES, &maps.w, kb * BK, item.m_blk * BM, item.e, &full[stage]);
-                    tma_load_2d(sB + stage * B_BYTES, &maps.x[mi], kb * BK, item.t0, &full[stage]);
+                    tma_load_3d(sA + stage * A_BYTES, &maps.w, kb * BKE, item.m_blk * BM, item.e, &full[stage]);
+                    tma_load_2d(sB + stage * B_BYTES, &maps.x[mi], kb * BKE, item.t0, &full[stage]);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -230,16 +251,21 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
                 mbar_wait(&tempty[acc], aphase ^ 1);
                 tc_fence_after();
                 const int nmma = (item.n + 15) & ~15;
-                const uint32_t idesc = idesc_bf16(nmma);
+                const uint32_t idesc = FP8 ? idesc_e4m3(nmma) : idesc_bf16(nmma);
                 const uint32_t dcol = tmem_base + static_cast<uint32_t>(acc * MAXN_T);
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B_BYTES);
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k)
-                        umma_bf16(dcol, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc,
-                                  (kb | k) != 0 ? 1u : 0u);
+                    for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of K per 128-byte row
+                        if (FP8)
+                            umma_e4m3(dcol, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc,
+                                      (kb | k) != 0 ? 1u : 0u);
+                        else
+                            umma_bf16(dcol, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc,
+                                      (kb | k) != 0 ? 1u : 0u);
+                    }
                     umma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
                     if (++stage == STAGES) {
                         stage = 0;
@@ -259,6 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             mbar_wait(&tfull[acc], aphase);
             tc_fence_after();
             const int row = item.m_blk * BM + warp * 32 + lane;
+            const float ws = FP8 ? __ldg(p.w_scale + item.e * p.mblocks + item.m_blk) : 1.0f;
             const uint32_t tbase = tmem_base + static_cast<uint32_t>(acc * MAXN_T) + (static_cast<uint32_t>(warp * 32) << 16);
             for (int c = 0; c < item.n; c += 32) {
                 uint32_t v[32];
@@ -267,9 +294,11 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
                 const int lim = min(32, item.n - c);
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
-                    if (j < lim)
-                        p.Y[static_cast<int64_t>(item.t0 + c + j) * p.ldy + row] =
-                            __float2bfloat16_rn(__uint_as_float(v[j]));
+                    if (j < lim) {
+                        float y = __uint_as_float(v[j]);
+                        if (FP8) y *= ws * __ldg(p.x_scale + item.t0 + c + j);
+                        p.Y[static_cast<int64_t>(item.t0 + c + j) * p.ldy + row] = __float2bfloat16_rn(y);
+                    }
             }
             tc_fence_before();
             __syncwarp();
@@ -297,6 +326,72 @@ __global__ void silu_mul_kernel(const __nv_bfloat16 *__restrict__ gu, int T, int
         const float g = __bfloat162float(gu[t * 2 * I + i]);
         const float u = __bfloat162float(gu[t * 2 * I + I + i]);
         h[idx] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u);
+    }
+}
+
+// FP8 (E4M3) rows with one scale per row: q[t, :] = e4m3(v[t, :] / s_t),
+// s_t = max |v[t, :]| / 448 (1 for an all-zero row).  One 256-thread CTA per row
+// (grid-stride over rows): each thread keeps its <= kQPairs element pairs in
+// registers, the row's max is a block reduction, and the E4M3 pairs are written
+// from registers -- one read of the row.
+constexpr int kQThreads = 256, kQPairs = 16;
+__device__ __forceinline__ uint16_t e4m3x2(float a, float b) {
+    return static_cast<uint16_t>(__nv_cvt_float2_to_fp8x2(make_float2(a, b), __NV_SATFINITE, __NV_E4M3));
+}
+__device__ __forceinline__ float block_max(float v, float *red) {
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, d));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();  // red is reused row after row
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    float m = red[0];
+#pragma unroll
+    for (int w = 1; w < kQThreads / 32; ++w) m = fmaxf(m, red[w]);
+    return m;
+}
+// MODE 0: v = x[t, :] (bf16 [T, K]); MODE 1: v = silu(gu[t, :K]) * gu[t, K:] (bf16 [T, 2K])
+template <int MODE>
+__global__ void __launch_bounds__(kQThreads) quantize_fp8_kernel(const __nv_bfloat16 *__restrict__ src, int T, int K,
+                                                                 uint8_t *__restrict__ q, float *__restrict__ qs,
+                                                                 const int32_t *rows_dev) {
+    __shared__ float red[kQThreads / 32];
+    pdl_wait();
+    pdl_launch_dependents();  // only once this kernel runs: at most one dependent waits
+    if (rows_dev) T = min(T, *rows_dev);
+    const int pairs = K / 2;
+    auto value = [&](int64_t t, int i) -> float2 {
+        if (MODE == 0) return __bfloat1622float2(reinterpret_cast<const __nv_bfloat162 *>(src + t * K)[i]);
+        const float2 g = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162 *>(src + t * 2 * K)[i]);
+        const float2 u = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162 *>(src + t * 2 * K + K)[i]);
+        return make_float2(g.x / (1.0f + __expf(-g.x)) * u.x, g.y / (1.0f + __expf(-g.y)) * u.y);
+    };
+    for (int64_t t = blockIdx.x; t < T; t += gridDim.x) {
+        float2 v[kQPairs];
+        float m = 0.0f;
+#pragma unroll
+        for (int j = 0; j < kQPairs; ++j) {
+            const int i = threadIdx.x + j * kQThreads;
+            v[j] = i < pairs ? value(t, i) : make_float2(0.0f, 0.0f);
+            m = fmaxf(m, fmaxf(fabsf(v[j].x), fabsf(v[j].y)));
+        }
+        for (int i = threadIdx.x + kQPairs * kQThreads; i < pairs; i += kQThreads) {  // rows beyond the registers
+            const float2 w = value(t, i);
+            m = fmaxf(m, fmaxf(fabsf(w.x), fabsf(w.y)));
+        }
+        m = block_max(m, red);
+        const float sc = m > 0.0f ? m / 448.0f : 1.0f, inv = 1.0f / sc;
+        uint16_t *out = reinterpret_cast<uint16_t *>(q + t * K);
+#pragma unroll
+        for (int j = 0; j < kQPairs; ++j) {
+            const int i = threadIdx.x + j * kQThreads;
+            if (i < pairs) out[i] = e4m3x2(v[j].x * inv, v[j].y * inv);
+        }
+        for (int i = threadIdx.x + kQPairs * kQThreads; i < pairs; i += kQThreads) {
+            const float2 w = value(t, i);
+            out[i] = e4m3x2(w.x * inv, w.y * inv);
+        }
+        if (threadIdx.x == 0) qs[t] = sc;
     }
 }
 
@@ -417,11 +512,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 static bool encode(CUtensorMap *m, void *base, int rank, const cuuint64_t *dims, const cuuint64_t *strides,
-                   const cuuint32_t *box) {
+                   const cuuint32_t *box, bool fp8 = false) {
     auto fn = encode_fn();
     if (!fn) return false;
     const cuuint32_t es[3] = {1, 1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, base, dims, strides, box, es,
+    return fn(m, fp8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, base, dims, strides,
+              box, es,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -434,26 +530,32 @@ extern "C" {
 
 static int launch_gemm(const void *W, int32_t E, int32_t M, int32_t K, const void *X, int32_t T,
                        const int32_t *items, int32_t n_items, const int32_t *n_items_dev, int32_t max_item_tokens,
-                       void *Y, int32_t num_ctas, void *stream) {
+                       void *Y, int32_t num_ctas, void *stream, const float *w_scale = nullptr,
+                       const float *x_scale = nullptr) {
+    const bool fp8 = w_scale != nullptr;
+    const cuuint64_t es = fp8 ? 1 : 2;             // bytes per element
+    const cuuint32_t bke = fp8 ? 2 * BK : BK;      // elements per 128-byte row
     Maps maps;
     const cuuint64_t wdims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(E)};
-    const cuuint64_t wstr[2] = {static_cast<cuuint64_t>(K) * 2, static_cast<cuuint64_t>(M) * K * 2};
-    const cuuint32_t wbox[3] = {BK, BM, 1};
-    if (!encode(&maps.w, const_cast<void *>(W), 3, wdims, wstr, wbox)) return METRO_ECUDA;
+    const cuuint64_t wstr[2] = {static_cast<cuuint64_t>(K) * es, static_cast<cuuint64_t>(M) * K * es};
+    const cuuint32_t wbox[3] = {bke, BM, 1};
+    if (!encode(&maps.w, const_cast<void *>(W), 3, wdims, wstr, wbox, fp8)) return METRO_ECUDA;
     const cuuint64_t xdims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(T)};
-    const cuuint64_t xstr[1] = {static_cast<cuuint64_t>(K) * 2};
+    const cuuint64_t xstr[1] = {static_cast<cuuint64_t>(K) * es};
     for (int i = 0; i < NMAPS; ++i) {
-        const cuuint32_t xbox[2] = {BK, static_cast<cuuint32_t>(16 << i)};
-        if (!encode(&maps.x[i], const_cast<void *>(X), 2, xdims, xstr, xbox)) return METRO_ECUDA;
+        const cuuint32_t xbox[2] = {bke, static_cast<cuuint32_t>(16 << i)};
+        if (!encode(&maps.x[i], const_cast<void *>(X), 2, xdims, xstr, xbox, fp8)) return METRO_ECUDA;
     }
     static std::once_flag attr;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(attr, [] {
-        attr_err = cudaFuncSetAttribute(moe_gemm_kernel<WideTile>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        WideTile::kSmem);
-        if (attr_err == cudaSuccess)
-            attr_err = cudaFuncSetAttribute(moe_gemm_kernel<NarrowTile>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            NarrowTile::kSmem);
+        const void *ks[4] = {reinterpret_cast<const void *>(moe_gemm_kernel<WideTile, false>),
+                             reinterpret_cast<const void *>(moe_gemm_kernel<NarrowTile, false>),
+                             reinterpret_cast<const void *>(moe_gemm_kernel<WideTile, true>),
+                             reinterpret_cast<const void *>(moe_gemm_kernel<NarrowTile, true>)};
+        const int sm[4] = {WideTile::kSmem, NarrowTile::kSmem, WideTile::kSmem, NarrowTile::kSmem};
+        for (int i = 0; i < 4 && attr_err == cudaSuccess; ++i)
+            attr_err = cudaFuncSetAttribute(ks[i], cudaFuncAttributeMaxDynamicSharedMemorySize, sm[i]);
     });
     if (attr_err != cudaSuccess) {
         g_err = attr_err;
@@ -470,10 +572,18 @@ static int launch_gemm(const void *W, int32_t E, int32_t M, int32_t K, const voi
     prm.K = K;
     prm.Y = static_cast<__nv_bfloat16 *>(Y);
     prm.ldy = M;
+    prm.w_scale = w_scale;
+    prm.x_scale = x_scale;
+    prm.mblocks = M / BM;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const cudaError_t e = max_item_tokens <= NarrowTile::kN
-                              ? launch_pdl(moe_gemm_kernel<NarrowTile>, grid, kThreads, NarrowTile::kSmem, s, maps, prm)
-                              : launch_pdl(moe_gemm_kernel<WideTile>, grid, kThreads, WideTile::kSmem, s, maps, prm);
+    const bool narrow = max_item_tokens <= NarrowTile::kN;
+    cudaError_t e;
+    if (fp8)
+        e = narrow ? launch_pdl(moe_gemm_kernel<NarrowTile, true>, grid, kThreads, NarrowTile::kSmem, s, maps, prm)
+                   : launch_pdl(moe_gemm_kernel<WideTile, true>, grid, kThreads, WideTile::kSmem, s, maps, prm);
+    else
+        e = narrow ? launch_pdl(moe_gemm_kernel<NarrowTile, false>, grid, kThreads, NarrowTile::kSmem, s, maps, prm)
+                   : launch_pdl(moe_gemm_kernel<WideTile, false>, grid, kThreads, WideTile::kSmem, s, maps, prm);
     if (e != cudaSuccess) {
         g_err = e;
         return METRO_ECUDA;
@@ -514,6 +624,49 @@ METRO_API int moe_grouped_gemm_dev_v1(const void *W, int32_t E, int32_t M, int32
                                       int32_t T_cap, const int32_t *items, int32_t items_cap,
                                       const int32_t *n_items_dev, void *Y, int32_t num_ctas, void *stream) {
     return moe_grouped_gemm_dev_v2(W, E, M, K, X, T_cap, items, items_cap, n_items_dev, MAXN, Y, num_ctas, stream);
+}
+
+METRO_API int moe_grouped_gemm_fp8_v1(const void *W8, const float *w_scale, int32_t E, int32_t M, int32_t K,
+                                      const void *X8, const float *x_scale, int32_t T, const int32_t *items,
+                                      int32_t n_items, const int32_t *n_items_dev, int32_t max_item_tokens, void *Y,
+                                      int32_t num_ctas, void *stream) {
+    if (!W8 || !w_scale || !X8 || !x_scale || !Y || !items || E < 1 || M < BM || K < 2 * BK || T < 1 ||
+        n_items < 0 || max_item_tokens < 1 || max_item_tokens > MAXN)
+        return METRO_EARG;
+    if (M % BM || K % (2 * BK)) return METRO_EDIMS;
+    if (n_items == 0) return METRO_OK;
+    return launch_gemm(W8, E, M, K, X8, T, items, n_items, n_items_dev, max_item_tokens, Y, num_ctas, stream, w_scale,
+                       x_scale);
+}
+
+METRO_API int moe_quantize_rows_fp8_v1(const void *X, int32_t T, int32_t K, void *X8, float *x_scale,
+                                       const int32_t *rows_dev, void *stream) {
+    if (!X || !X8 || !x_scale || T < 0 || K < 2 || (K & 1)) return METRO_EARG;
+    if (T == 0) return METRO_OK;
+    const int grid = T < 148 * 8 ? T : 148 * 8;  // one CTA per row, grid-stride
+    const cudaError_t e = launch_pdl(quantize_fp8_kernel<0>, grid, kQThreads, 0, static_cast<cudaStream_t>(stream),
+                                     static_cast<const __nv_bfloat16 *>(X), static_cast<int>(T), static_cast<int>(K),
+                                     static_cast<uint8_t *>(X8), x_scale, rows_dev);
+    if (e != cudaSuccess) {
+        g_err = e;
+        return METRO_ECUDA;
+    }
+    return METRO_OK;
+}
+
+METRO_API int moe_silu_mul_fp8_v1(const void *GU, int32_t T, int32_t I, void *H8, float *h_scale,
+                                  const int32_t *rows_dev, void *stream) {
+    if (!GU || !H8 || !h_scale || T < 0 || I < 2 || (I & 1)) return METRO_EARG;
+    if (T == 0) return METRO_OK;
+    const int grid = T < 148 * 8 ? T : 148 * 8;
+    const cudaError_t e = launch_pdl(quantize_fp8_kernel<1>, grid, kQThreads, 0, static_cast<cudaStream_t>(stream),
+                                     static_cast<const __nv_bfloat16 *>(GU), static_cast<int>(T), static_cast<int>(I),
+                                     static_cast<uint8_t *>(H8), h_scale, rows_dev);
+    if (e != cudaSuccess) {
+        g_err = e;
+        return METRO_ECUDA;
+    }
+    return METRO_OK;
 }
 
 METRO_API int moe_layout_items_v1(const int32_t *rep_off, const int32_t *slot_base, int32_t rank, int32_t M1,

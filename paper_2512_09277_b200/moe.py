@@ -39,6 +39,12 @@ def _lib():
         L.moe_grouped_gemm_dev_v2.restype = ctypes.c_int
         L.moe_item_tokens.argtypes = []
         L.moe_item_tokens.restype = ctypes.c_int32
+        L.moe_grouped_gemm_fp8_v1.argtypes = [P, P, i32, i32, i32, P, P, i32, P, i32, P, i32, P, i32, P]
+        L.moe_grouped_gemm_fp8_v1.restype = ctypes.c_int
+        L.moe_quantize_rows_fp8_v1.argtypes = [P, i32, i32, P, P, P, P]
+        L.moe_quantize_rows_fp8_v1.restype = ctypes.c_int
+        L.moe_silu_mul_fp8_v1.argtypes = [P, i32, i32, P, P, P, P]
+        L.moe_silu_mul_fp8_v1.restype = ctypes.c_int
         L.moe_silu_mul_v1.argtypes = [P, i32, i32, P, P]
         L.moe_silu_mul_v1.restype = ctypes.c_int
         L.moe_grouped_gemm_dev_v1.argtypes = [P, i32, i32, i32, P, i32, P, i32, P, P, i32, P]
@@ -157,17 +163,103 @@ def rank_workload_eplb(x: np.ndarray, A: np.ndarray, rank: int) -> RankWorkload:
     return RankWorkload(groups, t, len(groups))
 
 
-class ExpertFFN:
-    """The experts hosted by one EP rank (bf16, random init: no checkpoints)."""
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
 
-    def __init__(self, slots: int, hidden: int, inter: int, device, seed: int = 0):
+
+def quantize_weights_fp8(W: torch.Tensor):
+    """bf16 W [E, M, K] -> (E4M3 bytes uint8 [E, M, K], f32 scale [E, M / 128]):
+    one scale per (expert, 128-row block) = max |w| / 448 (weight loading, cold)."""
+    E, M, K = W.shape
+    if M % BM:
+        raise ValidationError(f"M={M} must be a multiple of {BM}")
+    blk = W.float().view(E, M // BM, BM, K)
+    s = (blk.abs().amax(dim=(2, 3)) / 448.0).clamp_min(torch.finfo(torch.float32).tiny)
+    q = (blk / s[:, :, None, None]).to(torch.float8_e4m3fn).view(torch.uint8).view(E, M, K)
+    return q.contiguous(), s.contiguous()
+
+
+def dequantize_fp8(q: torch.Tensor, scale: torch.Tensor, rows_per_scale: int) -> torch.Tensor:
+    """E4M3 bytes + scales -> f32 (test reference)."""
+    v = q.view(torch.float8_e4m3fn).float()
+    return v * scale.repeat_interleave(rows_per_scale, dim=-1)[..., None]
+
+
+def quantize_rows_fp8(X: torch.Tensor, X8: torch.Tensor = None, xs: torch.Tensor = None, rows_dev=None):
+    """bf16 [T, K] -> (E4M3 uint8 [T, K], f32 [T]) with one scale per row (device)."""
+    T, K = X.shape
+    if X8 is None:
+        X8 = torch.empty((T, K), dtype=torch.uint8, device=X.device)
+    if xs is None:
+        xs = torch.empty(T, dtype=torch.float32, device=X.device)
+    _check(_lib().moe_quantize_rows_fp8_v1(X.data_ptr(), T, K, X8.data_ptr(), xs.data_ptr(),
+                                            None if rows_dev is None else rows_dev.data_ptr(),
+                                            _stream_ptr(X.device)), "moe_quantize_rows_fp8_v1")
+    return X8, xs
+
+
+def silu_mul_fp8(GU: torch.Tensor, H8: torch.Tensor = None, hs: torch.Tensor = None, rows_dev=None):
+    """silu(gate) * up of GU [T, 2I] (bf16) -> (E4M3 uint8 [T, I], f32 [T])."""
+    T, I2 = GU.shape
+    I = I2 // 2
+    if H8 is None:
+        H8 = torch.empty((T, I), dtype=torch.uint8, device=GU.device)
+    if hs is None:
+        hs = torch.empty(T, dtype=torch.float32, device=GU.device)
+    _check(_lib().moe_silu_mul_fp8_v1(GU.data_ptr(), T, I, H8.data_ptr(), hs.data_ptr(),
+                                       None if rows_dev is None else rows_dev.data_ptr(),
+                                       _stream_ptr(GU.device)), "moe_silu_mul_fp8_v1")
+    return H8, hs
+
+
+def grouped_gemm_fp8(W8: torch.Tensor, w_scale: torch.Tensor, X8: torch.Tensor, x_scale: torch.Tensor, items,
+                     Y: torch.Tensor = None, num_ctas: int = 0, max_item_tokens: int = None,
+                     n_items_dev: torch.Tensor = None) -> torch.Tensor:
+    """Y[t, m] = w_scale[e, m / 128] * x_scale[t] * sum_k W8[e][m, k] X8[t, k] (E4M3 in, bf16 out)."""
+    if W8.dtype != torch.uint8 or X8.dtype != torch.uint8:
+        raise ValidationError("W8 and X8 must be E4M3 bytes (uint8)")
+    E, M, K = W8.shape
+    T = X8.shape[0]
+    if max_item_tokens is None:
+        if isinstance(items, np.ndarray) or (isinstance(items, torch.Tensor) and not items.is_cuda):
+            a = np.asarray(items).reshape(-1, 4)
+            max_item_tokens = int(a[:, 3].max()) if len(a) else 1
+        else:
+            max_item_tokens = MAXN
+    items = torch.as_tensor(np.asarray(items).reshape(-1, 4) if isinstance(items, np.ndarray) else items)
+    items = items.to(device=W8.device, dtype=torch.int32).contiguous()
+    if Y is None:
+        Y = torch.empty((T, M), dtype=torch.bfloat16, device=W8.device)
+    rc = _lib().moe_grouped_gemm_fp8_v1(W8.data_ptr(), w_scale.data_ptr(), E, M, K, X8.data_ptr(),
+                                        x_scale.data_ptr(), T, items.data_ptr(), items.shape[0],
+                                        None if n_items_dev is None else n_items_dev.data_ptr(),
+                                        int(max_item_tokens), Y.data_ptr(), num_ctas, _stream_ptr(W8.device))
+    _check(rc, "moe_grouped_gemm_fp8_v1")
+    return Y
+
+
+class ExpertFFN:
+    """The experts hosted by one EP rank (random init: no checkpoints).
+
+    ``dtype`` "bf16" or "fp8" (E4M3 weights with a scale per 128-row block, E4M3
+    activations with a scale per token: DeepSeek-V3 ships FP8 experts)."""
+
+    def __init__(self, slots: int, hidden: int, inter: int, device, seed: int = 0, dtype: str = "bf16"):
+        if dtype not in ("bf16", "fp8"):
+            raise ValidationError(f"unknown expert dtype {dtype!r}")
         g = torch.Generator(device=device).manual_seed(seed)
-        self.slots, self.hidden, self.inter = slots, hidden, inter
+        self.slots, self.hidden, self.inter, self.dtype = slots, hidden, inter, dtype
         self.W1 = (torch.randn((slots, 2 * inter, hidden), generator=g, device=device) * hidden ** -0.5).to(torch.bfloat16)
         self.W2 = (torch.randn((slots, hidden, inter), generator=g, device=device) * inter ** -0.5).to(torch.bfloat16)
+        if dtype == "fp8":
+            self.W1q, self.W1s = quantize_weights_fp8(self.W1)
+            self.W2q, self.W2s = quantize_weights_fp8(self.W2)
+            del self.W1, self.W2  # the FP8 copies are the weights
+            self.W1 = self.W2 = None
 
     def weight_bytes(self, activated: int) -> int:
-        return activated * (self.W1[0].numel() + self.W2[0].numel()) * 2
+        per = 2 * self.inter * self.hidden + self.hidden * self.inter
+        return activated * per * (1 if self.dtype == "fp8" else 2)
 
     def plan(self, wl: RankWorkload, device):
         it1 = torch.from_numpy(build_items(wl.groups, 2 * self.inter)).to(device)
@@ -176,6 +268,17 @@ class ExpertFFN:
 
     def forward(self, X: torch.Tensor, items1: torch.Tensor, items2: torch.Tensor, bufs=None) -> torch.Tensor:
         T = X.shape[0]
+        if self.dtype == "fp8":
+            nt = item_tokens()
+            if bufs is None:
+                bufs = (torch.empty((T, 2 * self.inter), dtype=torch.bfloat16, device=X.device),
+                        None, torch.empty((T, self.hidden), dtype=torch.bfloat16, device=X.device))
+            GU, _, Y = bufs
+            X8, xs = quantize_rows_fp8(X)
+            grouped_gemm_fp8(self.W1q, self.W1s, X8, xs, items1, GU, max_item_tokens=nt)
+            H8, hs = silu_mul_fp8(GU)
+            grouped_gemm_fp8(self.W2q, self.W2s, H8, hs, items2, Y, max_item_tokens=nt)
+            return Y
         if bufs is None:
             bufs = (torch.empty((T, 2 * self.inter), dtype=torch.bfloat16, device=X.device),
                     torch.empty((T, self.inter), dtype=torch.bfloat16, device=X.device),
@@ -234,6 +337,12 @@ class RankMoE:
         self.GU = torch.empty((self.rows_cap, 2 * ffn.inter), **bf)
         self.H = torch.empty((self.rows_cap, ffn.inter), **bf)
         self.Y = torch.empty((self.rows_cap, ffn.hidden), **bf)
+        if ffn.dtype == "fp8":  # E4M3 rows + per-row scales of the GEMM inputs
+            u8 = dict(dtype=torch.uint8, device=dev)
+            self.X8 = torch.empty((self.rows_cap, ffn.hidden), **u8)
+            self.xs = torch.empty(self.rows_cap, dtype=torch.float32, device=dev)
+            self.H8 = torch.empty((self.rows_cap, ffn.inter), **u8)
+            self.hs = torch.empty(self.rows_cap, dtype=torch.float32, device=dev)
 
     def __call__(self, topk_ids: torch.Tensor, hidden: torch.Tensor, stream=None) -> torch.Tensor:
         """topk_ids int32 [B, k] (all-gathered), hidden bf16 [B, D] -> Y [rows_cap, D]
@@ -262,6 +371,21 @@ class RankMoE:
                "moe_gather_rows_v1")
         f = self.ffn
         nt = item_tokens()  # moe_layout_items_v1 chunks at this many tokens
+        if f.dtype == "fp8":
+            rows = self.counts[2:].data_ptr()
+            _check(L.moe_quantize_rows_fp8_v1(self.X.data_ptr(), self.rows_cap, f.hidden, self.X8.data_ptr(),
+                                              self.xs.data_ptr(), rows, sp), "moe_quantize_rows_fp8_v1")
+            _check(L.moe_grouped_gemm_fp8_v1(f.W1q.data_ptr(), f.W1s.data_ptr(), f.slots, 2 * f.inter, f.hidden,
+                                             self.X8.data_ptr(), self.xs.data_ptr(), self.rows_cap,
+                                             self.items1.data_ptr(), self.cap1, self.counts.data_ptr(), nt,
+                                             self.GU.data_ptr(), 0, sp), "moe_grouped_gemm_fp8_v1")
+            _check(L.moe_silu_mul_fp8_v1(self.GU.data_ptr(), self.rows_cap, f.inter, self.H8.data_ptr(),
+                                         self.hs.data_ptr(), rows, sp), "moe_silu_mul_fp8_v1")
+            _check(L.moe_grouped_gemm_fp8_v1(f.W2q.data_ptr(), f.W2s.data_ptr(), f.slots, f.hidden, f.inter,
+                                             self.H8.data_ptr(), self.hs.data_ptr(), self.rows_cap,
+                                             self.items2.data_ptr(), self.cap2, self.counts[1:].data_ptr(), nt,
+                                             self.Y.data_ptr(), 0, sp), "moe_grouped_gemm_fp8_v1")
+            return self.Y
         _check(L.moe_grouped_gemm_dev_v2(f.W1.data_ptr(), f.slots, 2 * f.inter, f.hidden, self.X.data_ptr(),
                                          self.rows_cap, self.items1.data_ptr(), self.cap1,
                                          self.counts.data_ptr(), nt, self.GU.data_ptr(), 0, sp),

@@ -201,3 +201,91 @@ def test_rank_moe_pipeline_on_device(kind):
         g.replay()
         torch.cuda.synchronize()
         assert torch.equal(pipe.Y[:rows], y0)
+
+
+# ------------------------------------------------------------------ FP8 (E4M3)
+@pytest.mark.parametrize("E,M,K,sizes", [
+    (3, 256, 512, [1, 17, 40, 300]),
+    (2, 384, 1024, [64, 65, 5]),
+])
+def test_grouped_gemm_fp8_vs_torch(E, M, K, sizes):
+    """E4M3 weights (scale per 128-row block) and activations (scale per row):
+    the kernel against a torch fp32 GEMM of the same dequantised values."""
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(E * 7 + M + K)
+    groups, t = [], 0
+    for i, n in enumerate(sizes):
+        groups.append((i % E, t, n))
+        t += n
+    W = (torch.randn((E, M, K), generator=g, device=dev) * K ** -0.5).to(torch.bfloat16)
+    X = torch.randn((t, K), generator=g, device=dev).to(torch.bfloat16)
+    W8, ws = moe.quantize_weights_fp8(W)
+    X8, xs = moe.quantize_rows_fp8(X)
+    torch.cuda.synchronize()
+    Wd = moe.dequantize_fp8(W8, ws, moe.BM)
+    Xd = X8.view(torch.float8_e4m3fn).float() * xs[:, None]
+    ref = torch.zeros((t, M), dtype=torch.float32, device=dev)
+    for e, t0, n in groups:
+        ref[t0:t0 + n] = Xd[t0:t0 + n] @ Wd[e].t()
+    for items in (moe.build_items(groups, M), wide_items(groups, M, 256)):
+        Y = moe.grouped_gemm_fp8(W8, ws, X8, xs, items)
+        torch.cuda.synchronize()
+        torch.testing.assert_close(Y.float(), ref, rtol=RTOL, atol=ATOL)
+    # the quantisation itself: |x - dequant(x)| within half an E4M3 step (3 mantissa bits)
+    err = (Xd - X.float()).abs()
+    assert bool((err <= X.float().abs() * 2.0 ** -4 + xs[:, None] * 2.0 ** -9).all())
+
+
+def test_silu_mul_fp8():
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(5)
+    T, I = 37, 512
+    GU = torch.randn((T, 2 * I), generator=g, device=dev).to(torch.bfloat16)
+    H8, hs = moe.silu_mul_fp8(GU)
+    torch.cuda.synchronize()
+    gf, uf = GU[:, :I].float(), GU[:, I:].float()
+    ref = gf * torch.sigmoid(gf) * uf
+    Hd = H8.view(torch.float8_e4m3fn).float() * hs[:, None]
+    torch.testing.assert_close(hs, ref.abs().amax(dim=1) / 448.0, rtol=1e-5, atol=1e-7)
+    assert bool(((Hd - ref).abs() <= ref.abs() * 2.0 ** -4 + hs[:, None] * 2.0 ** -9 + 1e-6).all())
+
+
+def test_rank_moe_fp8_matches_host_plan():
+    """The device pipeline (route -> layout -> items -> gather -> quantise -> FP8
+    GEMMs) equals the same rank's FFN run from host-planned items."""
+    from paper_2512_09277_b200 import DevicePlacement
+    from paper_2512_09277_b200.placement import gen_zipf_topk, make_placement
+
+    dev = torch.device("cuda")
+    N, k, G, B, D, I = 64, 4, 4, 96, 256, 128
+    A = make_placement(N, G, 1.5, 7).matrix
+    pl = DevicePlacement(A, dev)
+    slots = int(A.sum(axis=0).max())
+    ids = torch.from_numpy(gen_zipf_topk(N, k, B, 1.2, 3, popularity_seed=7)).to(dev)
+    g = torch.Generator(device=dev).manual_seed(11)
+    hidden = torch.randn((B, D), generator=g, device=dev).to(torch.bfloat16)
+    for rank in range(G):
+        ffn = moe.ExpertFFN(slots, D, I, dev, seed=rank, dtype="fp8")
+        pipe = moe.RankMoE(pl, "metro", rank, ffn, max_pairs=B * k, top_k=k)
+        Y = pipe(ids, hidden)
+        torch.cuda.synchronize()
+        rows = int(pipe.counts[2].item())
+        # host reference of the same rank: its received rows in layout order, host items
+        X = pipe.X[:rows].clone()
+        lo = pipe.layout_out
+        rep_off = lo.rep_off.cpu().numpy()
+        sb = pipe.layout.slot_base.cpu().numpy()
+        groups = []
+        base = rep_off[sb[rank]]
+        for sl in range(sb[rank + 1] - sb[rank]):
+            n = int(rep_off[sb[rank] + sl + 1] - rep_off[sb[rank] + sl])
+            if n:
+                groups.append((sl, int(rep_off[sb[rank] + sl] - base), n))
+        if not groups:
+            assert rows == 0
+            continue
+        i1 = moe.build_items(groups, 2 * I)
+        i2 = moe.build_items(groups, D)
+        Yh = ffn.forward(X, torch.from_numpy(i1).to(dev), torch.from_numpy(i2).to(dev))
+        torch.cuda.synchronize()
+        torch.testing.assert_close(Y[:rows].float(), Yh.float(), rtol=0, atol=0)

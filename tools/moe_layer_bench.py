@@ -71,14 +71,15 @@ def time_graph(fn, reps, inner=1):
     return statistics.median(ts)
 
 
-def run(batches=4, reps=5, B=1024, ratio=1.5, seed0=1000):
+def run(batches=4, reps=5, B=1024, ratio=1.5, seed0=1000, dtype="bf16"):
     dev = torch.device("cuda", 0)
     N, k, G = 256, 8, 8
     A = make_placement(N, G, ratio, 7).matrix
     slots = int(A.sum(axis=0).max())
     pl = DevicePlacement(A, dev)
     rm, re_ = Router(pl, "metro"), Router(pl, "eplb")
-    ffn = moe.ExpertFFN(slots, HIDDEN, INTER, dev, seed=0)
+    ffn = moe.ExpertFFN(slots, HIDDEN, INTER, dev, seed=0, dtype=dtype)
+    eb = 1 if dtype == "fp8" else 2  # bytes per GEMM input element
     pk, pk_src = peak_gbs()
     rows = []
     for b in range(batches):
@@ -100,7 +101,8 @@ def run(batches=4, reps=5, B=1024, ratio=1.5, seed0=1000):
                     torch.empty((X.shape[0], HIDDEN), dtype=torch.bfloat16, device=dev))
             us = time_ffn(ffn, X, i1, i2, bufs, reps)
             wbytes = ffn.weight_bytes(wl.activated)
-            abytes = wl.tokens * (HIDDEN + 2 * INTER + INTER + INTER + HIDDEN) * 2
+            # activations: X in, GU out + in (bf16), H in, Y out (bf16)
+            abytes = wl.tokens * (HIDDEN * eb + 2 * INTER * 2 * 2 + INTER * eb + HIDDEN * 2)
             res[kind] = {"rank": g, "activated": wl.activated, "tokens": wl.tokens, "ffn_us": us,
                          "weight_bytes": wbytes, "achieved_gbs": (wbytes + abytes) / (us * 1e-6) / 1e9}
             res[kind]["frac"] = res[kind]["achieved_gbs"] / pk
@@ -124,13 +126,14 @@ def run(batches=4, reps=5, B=1024, ratio=1.5, seed0=1000):
         summ[kind] = {key: statistics.mean(r[kind][key] for r in rows)
                       for key in ("activated", "tokens", "ffn_us", "weight_bytes", "achieved_gbs", "frac",
                                   "device_layer_us", "dispatch_layout_us")}
+    summ["dtype"] = dtype
     summ["ffn_speedup_metro_vs_eplb"] = summ["eplb"]["ffn_us"] / summ["metro"]["ffn_us"]
     summ["device_layer_speedup_metro_vs_eplb"] = summ["eplb"]["device_layer_us"] / summ["metro"]["device_layer_us"]
     summ["weight_byte_ratio_eplb_over_metro"] = summ["eplb"]["weight_bytes"] / summ["metro"]["weight_bytes"]
     summ["peak_gbs"] = pk
     summ["peak_source"] = pk_src
     summ["shape"] = {"experts": N, "top_k": k, "ep_ranks": G, "replication": ratio, "batch": B,
-                     "hidden": HIDDEN, "intermediate": INTER, "dtype": "bf16", "slots_per_rank": slots}
+                     "hidden": HIDDEN, "intermediate": INTER, "dtype": dtype, "slots_per_rank": slots}
     return summ
 
 
@@ -140,8 +143,9 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--batch", type=int, default=1024)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp8"])
     a = ap.parse_args()
-    s = run(a.batches, a.reps, a.batch)
+    s = run(a.batches, a.reps, a.batch, dtype=a.dtype)
     print(json.dumps(s))
     if a.json:
         with open(a.json, "w") as f:
