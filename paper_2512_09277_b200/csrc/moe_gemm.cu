@@ -314,18 +314,21 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
 }
 
 // H[t, i] = silu(GU[t, i]) * GU[t, I + i]   (gate | up halves of the first projection)
+// One CTA per row (grid-stride over rows), bf16 pairs: no per-element division.
 __global__ void silu_mul_kernel(const __nv_bfloat16 *__restrict__ gu, int T, int I, __nv_bfloat16 *__restrict__ h,
                                 const int32_t *rows_dev) {
     pdl_wait();
     pdl_launch_dependents();  // only once this kernel runs: at most one dependent waits
     if (rows_dev) T = min(T, *rows_dev);
-    const int64_t total = static_cast<int64_t>(T) * I;
-    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
-         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t t = idx / I, i = idx - t * I;
-        const float g = __bfloat162float(gu[t * 2 * I + i]);
-        const float u = __bfloat162float(gu[t * 2 * I + I + i]);
-        h[idx] = __float2bfloat16_rn(g / (1.0f + __expf(-g)) * u);
+    const int pairs = I / 2;
+    for (int64_t t = blockIdx.x; t < T; t += gridDim.x) {
+        const __nv_bfloat162 *g = reinterpret_cast<const __nv_bfloat162 *>(gu + t * 2 * I);
+        const __nv_bfloat162 *u = reinterpret_cast<const __nv_bfloat162 *>(gu + t * 2 * I + I);
+        __nv_bfloat162 *o = reinterpret_cast<__nv_bfloat162 *>(h + t * I);
+        for (int i = threadIdx.x; i < pairs; i += blockDim.x) {
+            const float2 a = __bfloat1622float2(g[i]), b = __bfloat1622float2(u[i]);
+            o[i] = __floats2bfloat162_rn(a.x / (1.0f + __expf(-a.x)) * b.x, a.y / (1.0f + __expf(-a.y)) * b.y);
+        }
     }
 }
 
@@ -406,6 +409,9 @@ __global__ void __launch_bounds__(kItThreads) layout_items_kernel(const int32_t 
                                                                   int mb1, int mb2, Item *items1, Item *items2,
                                                                   int cap1, int cap2, int32_t *counts) {
     __shared__ int32_t s_w[32];
+    // per slot of the current chunk of kItThreads slots: first chunk (exclusive
+    // prefix within the chunk; [kItThreads] = the chunk's total), first row, rows
+    __shared__ int32_t s_pre[kItThreads + 1], s_t0[kItThreads], s_n[kItThreads];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     pdl_wait();
     pdl_launch_dependents();  // only once this kernel runs: at most one dependent waits
@@ -434,21 +440,36 @@ __global__ void __launch_bounds__(kItThreads) layout_items_kernel(const int32_t 
             s_w[lane] = w;
         }
         __syncthreads();
-        const int before = run + x - c + (warp > 0 ? s_w[warp - 1] : 0);
-        if (c > 0) {
-            const int t0 = rep_off[b0 + s] - base_row;
-            for (int mb = 0; mb < mb1; ++mb)
-                for (int j = 0; j < c; ++j) {
-                    const int idx = before * mb1 + mb * c + j;
-                    if (idx < cap1) items1[idx] = Item{s, mb, t0 + j * kItemTokens, min(kItemTokens, n - j * kItemTokens)};
+        const int chunk_total = s_w[kItThreads / 32 - 1];
+        s_pre[tid] = x - c + (warp > 0 ? s_w[warp - 1] : 0);
+        s_t0[tid] = (s < S) ? rep_off[b0 + s] - base_row : 0;
+        s_n[tid] = n;
+        if (tid == 0) s_pre[kItThreads] = chunk_total;
+        __syncthreads();
+        // every thread writes items: item q of this chunk belongs to the last slot
+        // whose first item (s_pre * mb) is <= q (binary search); items are slot-major,
+        // then (m_block, chunk) -- the order of moe.build_items
+        auto emit = [&](Item *items, int mb, int cap) {
+            const int tot = chunk_total * mb;
+            for (int q = tid; q < tot; q += kItThreads) {
+                int lo = 0, hi = kItThreads - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (s_pre[mid] * mb <= q) lo = mid;
+                    else hi = mid - 1;
                 }
-            for (int mb = 0; mb < mb2; ++mb)
-                for (int j = 0; j < c; ++j) {
-                    const int idx = before * mb2 + mb * c + j;
-                    if (idx < cap2) items2[idx] = Item{s, mb, t0 + j * kItemTokens, min(kItemTokens, n - j * kItemTokens)};
-                }
-        }
-        run += s_w[kItThreads / 32 - 1];
+                // skip empty slots that share the prefix (their range is empty)
+                const int cc = s_pre[lo + 1] - s_pre[lo];
+                const int local = q - s_pre[lo] * mb, m_blk = local / cc, j = local - m_blk * cc;
+                const int idx = (run + s_pre[lo]) * mb + local;
+                if (idx < cap)
+                    items[idx] = Item{s0 + lo, m_blk, s_t0[lo] + j * kItemTokens,
+                                      min(kItemTokens, s_n[lo] - j * kItemTokens)};
+            }
+        };
+        emit(items1, mb1, cap1);
+        if (mb2 > 0) emit(items2, mb2, cap2);
+        run += chunk_total;
         __syncthreads();
     }
     if (tid == 0) {
@@ -723,10 +744,9 @@ METRO_API int moe_silu_mul_dev_v1(const void *GU, int32_t T_cap, int32_t I, void
 }
 
 static int launch_silu(const void *GU, int32_t T, int32_t I, void *H, const int32_t *rows_dev, void *stream) {
-    if (!GU || !H || T < 0 || I < 1) return METRO_EARG;
+    if (!GU || !H || T < 0 || I < 2 || (I & 1)) return METRO_EARG;
     if (T == 0) return METRO_OK;
-    const int64_t total = static_cast<int64_t>(T) * I;
-    const int grid = static_cast<int>(total / 256 + 1 < 148 * 8 ? total / 256 + 1 : 148 * 8);
+    const int grid = T < 148 * 8 ? T : 148 * 8;  // one CTA per row, grid-stride
     const cudaError_t e = launch_pdl(silu_mul_kernel, grid, 256, 0, static_cast<cudaStream_t>(stream),
                                      static_cast<const __nv_bfloat16 *>(GU), static_cast<int>(T),
                                      static_cast<int>(I), static_cast<__nv_bfloat16 *>(H), rows_dev);

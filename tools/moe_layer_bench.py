@@ -35,17 +35,9 @@ def peak_gbs():
 
 
 def time_ffn(ffn, X, i1, i2, bufs, reps):
-    ffn.forward(X, i1, i2, bufs)  # warm
-    torch.cuda.synchronize()
-    ts = []
-    for _ in range(reps):
-        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-        e0.record()
-        ffn.forward(X, i1, i2, bufs)
-        e1.record()
-        torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1) * 1e3)
-    return statistics.median(ts)
+    """Device time of the rank's expert FFN (all its kernels captured in one CUDA
+    graph, so host launch gaps between them are not counted)."""
+    return time_graph(lambda st: ffn.forward(X, i1, i2, bufs), reps)
 
 
 def time_graph(fn, reps, inner=1):
