@@ -495,7 +495,17 @@ __global__ void gather_rows_kernel(const uint4 *__restrict__ src, int row_vecs, 
         if (r < 0 || r >= rows_cap) continue;
         const uint4 *s = src + (p / k) * row_vecs;
         uint4 *d = dst + static_cast<int64_t>(r) * row_vecs;
-        for (int v = lane; v < row_vecs; v += 32) d[v] = s[v];
+        // eight independent 16-byte loads in flight per lane before the stores
+        constexpr int U = 8;
+        int v0 = lane;
+        for (; v0 + (U - 1) * 32 < row_vecs; v0 += U * 32) {
+            uint4 t[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) t[u] = __ldg(s + v0 + u * 32);
+#pragma unroll
+            for (int u = 0; u < U; ++u) d[v0 + u * 32] = t[u];
+        }
+        for (int v = v0; v < row_vecs; v += 32) d[v] = __ldg(s + v);
     }
 }
 
