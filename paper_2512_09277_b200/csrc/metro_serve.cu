@@ -1,26 +1,25 @@
 // metro_serve.cu -- persistent end-to-end METRO router for host callers
 // (include/metro_serve.h).
 //
-// One resident CTA (512 threads) per server.  Thread 0 polls a doorbell word in
-// pinned host memory with system-scope acquire loads; the request names the
-// caller's pinned buffers.  The CTA then runs the same phases as one
-// metro_ids_kernel launch with R = 1 (metro_core.cuh): the ids are staged into
-// shared memory with system-scope 16-byte loads straight from host memory,
-// lane-striped histogram -> METRO decision (routing.py:105-113: order by
-// (r asc, T desc, id asc), greedy argmin with the ascending strict-'<' scan) ->
-// per-pair ranks, and the results are stored into the caller's host buffers.
-// Every thread fences at system scope, then thread 0 publishes the completion
-// word with a system-scope release store.  No kernel launch and no stream
-// synchronisation on the per-call path: the launch + sync floor of the
-// one-launch path (~9 us measured on the B200 box, tools/host_latency.cu) is
-// replaced by two PCIe round trips.
+// One resident CTA per server: 16 routing warps + 1-4 doorbell warps.  Lane 0 of
+// each doorbell warp keeps one system-scope acquire load of the doorbell word
+// (pinned host memory) in flight, the warps staggered; the first to see a new
+// request claims it and arrives on a named barrier the routing warps wait on.
+// The routing warps then run the phases of one metro_ids_kernel launch with
+// R = 1 (metro_core.cuh): the ids are read from host memory with system-scope
+// 16-byte loads and counted into the lane-striped histogram as they arrive,
+// METRO decision (routing.py:105-113: order by (r asc, T desc, id asc), greedy
+// argmin with the ascending strict-'<' scan) -> per-pair ranks, results stored
+// into the caller's pinned buffers, and thread 0 publishes the completion word
+// with a system-scope release store (cumulative over the CTA barrier).  No
+// kernel launch and no stream synchronisation on the per-call path: the launch
+// + sync floor of the one-launch path (~9 us measured on the B200 box,
+// tools/host_latency.cu) is replaced by two PCIe round trips.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 #include <time.h>
-
-#include <atomic>
 
 #include "../../include/metro_serve.h"
 #include "lib_internal.h"
@@ -53,11 +52,6 @@ constexpr uint32_t kSeqMask = 0xffffffu, kNewPtrs = 1u << 24;
 
 enum : uint32_t { kServeLaunched = 1, kServeIdleExit = 2, kServeStopped = 3 };
 
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
-    uint32_t v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 __device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t *p) {
     uint32_t v;
     asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -89,7 +83,6 @@ __device__ __forceinline__ int ld_relaxed_sys_s32(const int32_t *p) {
 __device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ uint64_t globaltimer_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
