@@ -186,6 +186,44 @@ def cpu_route_layers(A, batches, seconds: float, min_layers: int = 0):
     return el / n * 1e6, n, outs
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_per_layer_stats(A, batches, reps: int = 400):
+    """Median / p99 µs of single layers (perf_counter around each call) for the
+    oracle port's METRO layer and its EPLB counterpart (aggregate_loads +
+    route_eplb + EPLB pair ranks), one host thread."""
+    import oracle
+
+    def one(fn):
+        ts = []
+        for i in range(reps):
+            b = batches[i % len(batches)]
+            t0 = time.perf_counter()
+            fn(b)
+            ts.append((time.perf_counter() - t0) * 1e6)
+        ts.sort()
+        return {"median": ts[len(ts) // 2], "p99": ts[int(len(ts) * 0.99)], "reps": reps}
+
+    def eplb_layer(b):
+        T = oracle.aggregate_loads(b, A.shape[0])
+        oracle.route_eplb(T, A)
+        oracle.pair_rank_eplb(b, A)
+
+    for b in batches[:4]:
+        oracle.metro_layer(b, A)
+        eplb_layer(b)
+    return {"metro_layer_us": one(lambda b: oracle.metro_layer(b, A)), "eplb_layer_us": one(eplb_layer)}
+
+
 def cpu_allcores_throughput(A, batches, seconds: float = 2.0):
     """Independent layers on every host core (context only; one layer is serial)."""
     from concurrent.futures import ThreadPoolExecutor
@@ -239,7 +277,7 @@ def run_reference(args, cfg, rank: int, world: int):
         "config": dict(config_dict(args, cfg, world), l2="n/a (host CPU path)",
                        parallelism="single host thread, one layer per step"),
         "cpu_baseline": {"value": us, "unit": "us/layer", "cores": 1, "kind": "port", "sample": sample,
-                         "all_cores_layers_per_s": thr, "host_cores": cores},
+                         "all_cores_layers_per_s": thr, "host_cores": cores, "cpu_model": cpu_model()},
         "e2e": {"value": us, "unit": "us/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -396,6 +434,22 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
             tf = loop_ms(Kb, lambda i: None, True)
             tr = loop_ms(Kb, route_base, True)
             method["after_flush_eager_us"] = (tr - tf) / Kb * 1e3
+            # single launches one at a time (events around each, stream idle before):
+            # the latency distribution of one layer's routing, launch included
+            single = []
+            for i in range(500):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record()
+                route_base(i)
+                e1.record()
+                torch.cuda.synchronize()
+                single.append(e0.elapsed_time(e1) * 1e3)
+            single.sort()
+            method["single_launch_us"] = {"mean": statistics.mean(single), "p50": single[len(single) // 2],
+                                          "p99": single[int(len(single) * 0.99)], "samples": len(single),
+                                          "note": "events around one eager launch on an idle stream: includes "
+                                                  "the host launch path (Python, ctypes, driver)"}
         else:
             # every step: 256 MiB L2 flush, NCCL all-gather of the local top-k ids,
             # routing kernel on the gathered batch; the flush-only loop is
@@ -615,7 +669,8 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
             "value": us, "unit": "us/layer", "cores": 1, "kind": "port",
             "sample": f"{layers} layers ({args.cpu_seconds:.0f} s) of this workload through the oracle "
                       "port (aggregate_loads + route_metro + pair_rank), single thread",
-            "all_cores_layers_per_s": thr, "host_cores": cores, "parity_vs_gpu": bool(parity),
+            "all_cores_layers_per_s": thr, "host_cores": cores, "cpu_model": cpu_model(),
+            "per_layer": cpu_per_layer_stats(A, batches), "parity_vs_gpu": bool(parity),
         }
     return res
 
