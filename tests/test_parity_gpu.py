@@ -315,3 +315,37 @@ def test_host_router_e2e(shapes):
         assert np.array_equal(out[8:8 + g], c["metro_counts"])
         assert np.array_equal(out[8 + g:8 + g + n], c["metro_choice"])
         assert np.array_equal(pr.numpy(), oracle.pair_rank_metro(c["ids"].reshape(-1), c["metro_choice"]))
+
+
+def test_pdl_chain_in_one_graph(shapes):
+    """Programmatic dependent launch inside a CUDA graph: each routing kernel
+    reads ids written by the kernel right before it (a copy kernel standing in
+    for the gating kernel), 64 layers back to back -- every layer must see its
+    own batch.  The same with PDL off."""
+    from paper_2512_09277_b200 import _native
+
+    cs = [s for s in shapes if s["name"] == "ds"]
+    pl = DevicePlacement(cs[0]["A"])
+    r = Router(pl, "metro")
+    src = [torch.from_numpy(s["ids"]).cuda() for s in cs]
+    L = 64
+    ids = torch.empty((L,) + tuple(src[0].shape), dtype=torch.int32, device="cuda")
+    outs = [r.alloc(src[0].numel(), top_k=8) for _ in range(L)]
+    for pdl in (1, 0):
+        _native.lib().metro_set_pdl(pdl)
+        try:
+            ids.zero_()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for j in range(L):
+                    ids[j].copy_(src[j % len(src)])  # the "producer" kernel of layer j
+                    r.route(ids[j], out=outs[j])
+            g.replay()
+            torch.cuda.synchronize()
+            for j in range(L):
+                s = cs[j % len(cs)]
+                assert np.array_equal(outs[j].choice.cpu().numpy(), s["metro_choice"]), (pdl, j)
+                assert int(outs[j].lam.item()) == s["metro_lam"]
+        finally:
+            _native.lib().metro_set_pdl(1)
