@@ -366,69 +366,66 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
     method = {}
     with ClockSampler(local_rank) as clk:
         if world == 1:
-            # (a) primary: back-to-back graph replays over a pool of distinct batches
-            # larger than L2 (rows resampled from the exact Zipf batches), so every
-            # step's ids come from HBM; one event pair around K launches.
+            # (a) primary: EXACTLY K launches, back to back from CUDA graphs, launch j on
+            # slot j % P of a pool of distinct batches larger than L2 (rows resampled
+            # from the exact Zipf batches).  Every graph is replayed once untimed (graph
+            # upload), then a 256 MiB flush empties L2, so every timed launch reads
+            # its ids from HBM (a slot recurs only P launches = 256 MiB later).
+            from paper_2512_09277_b200 import _native
+
             per_batch = B * k * 4
             P = max(256, -(-POOL_BYTES // per_batch))
             gen = torch.Generator(device=dev).manual_seed(1234)
             rows = torch.randint(0, POOL * B, (P, B), device=dev, generator=gen)
             big = base.reshape(POOL * B, k)[rows].contiguous()  # [P, B, k]
             chunk = 256
-            graphs = []
-            for c0 in range(0, P, chunk):
-                for j in range(c0, min(P, c0 + chunk)):  # warm each slot once
-                    router.route(big[j], out=out)
-                torch.cuda.synchronize()
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    for j in range(c0, min(P, c0 + chunk)):
-                        router.route(big[j], out=out)
-                graphs.append(g)
-            reps = max(1, -(-K // (P)))
-            n_launch = reps * P
-            graphs[0].replay()
-            sync_all()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            wall0 = time.perf_counter()
-            e0.record()
-            for _ in range(reps):
+
+            def build(n):
+                graphs = []
+                for c0 in range(0, n, chunk):
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g):
+                        for j in range(c0, min(n, c0 + chunk)):
+                            router.route(big[j % P], out=out)
+                    graphs.append(g)
+                return graphs
+
+            def timed(graphs, n):
+                for g in graphs:  # untimed: graph upload
+                    g.replay()
+                flush.zero_()
+                sync_all()
+                w0 = time.perf_counter()
+                e0.record()
                 for g in graphs:
                     g.replay()
-            e1.record()
-            torch.cuda.synchronize()
-            wall = time.perf_counter() - wall0
-            step_ms = e0.elapsed_time(e1) / n_launch
-            K_eff = n_launch
+                e1.record()
+                torch.cuda.synchronize()
+                return e0.elapsed_time(e1) / n, time.perf_counter() - w0
+
+            graphs = build(K)
+            step_ms, wall = timed(graphs, K)
+            del graphs
+            K_eff = K
             kern_ms = step_ms
             ag_ms = 0.0
-            method = {"method": "graph-replayed back-to-back over a {:.0f} MiB pool of {} distinct batches (> L2)"
-                      .format(P * per_batch / 2 ** 20, P),
+            method = {"method": "exactly K launches replayed back-to-back from CUDA graphs, launch j on slot j % {} "
+                                "of a {:.0f} MiB pool of distinct batches (> L2), L2 flushed before the timed "
+                                "replay".format(P, P * per_batch / 2 ** 20),
                       "pdl": "programmatic dependent launch: each routing kernel's shared-memory prologue "
                              "overlaps the previous kernel; it waits for that kernel's completion before "
                              "reading its ids (as behind the gating kernel in a decode step)"}
-            del graphs
-            # the same pool measurement with PDL off (every launch fully serialised)
-            from paper_2512_09277_b200 import _native
-
+            # the same measurement with PDL off (every launch fully serialised)
             _native.lib().metro_set_pdl(0)
-            graphs = []
-            for c0 in range(0, P, chunk):
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    for j in range(c0, min(P, c0 + chunk)):
-                        router.route(big[j], out=out)
-                graphs.append(g)
-            _native.lib().metro_set_pdl(1)
-            graphs[0].replay()
-            torch.cuda.synchronize()
-            e0.record()
-            for g in graphs:
-                g.replay()
-            e1.record()
-            torch.cuda.synchronize()
-            method["no_pdl_us"] = e0.elapsed_time(e1) / P * 1e3
-            del graphs, big
+            try:
+                n_np = min(K, 2048)
+                graphs = build(n_np)
+                method["no_pdl_us"] = timed(graphs, n_np)[0] * 1e3
+                del graphs
+            finally:
+                _native.lib().metro_set_pdl(1)
+            del big
             # (b) context: eager launch after a 256 MiB L2 flush, flush time subtracted
             Kb = min(K, 2000)
             tf = loop_ms(Kb, lambda i: None, True)
