@@ -135,3 +135,23 @@ def test_fused_allgather_missing_peer_times_out(monkeypatch):
     finally:
         for b in bufs:
             b.close()
+
+
+@pytest.mark.parametrize("world", [1, 4])
+def test_fused_allgather_empty_local_batches(world):
+    """No tokens anywhere: every rank reports an empty routing (λ 0), twice."""
+    A = make_placement(128, 8, 1.5, 7).matrix
+    pl = DevicePlacement(A)
+    routers, bufs = virtual_ranks(pl, world, 0, 8, gather_ids=True)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    try:
+        empty = [torch.zeros((0, 8), dtype=torch.int32, device="cuda") for _ in range(world)]
+        for _ in range(2):
+            run_all(routers, empty, streams)
+            for rt in routers:
+                rt.out.check()
+                assert int(rt.out.lam.item()) == 0
+                assert bool((rt.out.choice == -1).all())
+    finally:
+        for b in bufs:
+            b.close()

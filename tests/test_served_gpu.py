@@ -128,3 +128,12 @@ def test_served_idle_exit_relaunch():
             time.sleep(0.002)
             check(sr, gen_zipf_topk(256, 8, 1024, 1.2, 1100 + s, popularity_seed=7), A)
     assert sr.launches == 0  # closed
+
+
+def test_served_empty_batches():
+    A = make_placement(128, 8, 1.5, 7).matrix
+    pl = DevicePlacement(A)
+    with ServedRouter(pl, 0) as sr:  # a server sized for nothing still answers
+        out = sr.run(0)
+        assert int(out[0]) == 0 and int(out[4]) == 0
+        assert (out[8:8 + 8] == 0).all() and (out[8 + 8:] == -1).all()
