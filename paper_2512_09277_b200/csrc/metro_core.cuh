@@ -52,8 +52,9 @@ struct Params {
     int32_t *ids_out;
     int32_t score_bytes;  // > 0: the CTA's score rows are staged in smem (bytes per CTA)
     void *gate_ws;        // metro_gate_kernel: int64 T[N] + arrival counter, zero between launches
+    int32_t gate_tokens;  // metro_gate_kernel: tokens per CTA (<= kGateTokens)
 };
-constexpr int kGateTokens = 2 * kThreads / 32;  // tokens per CTA in metro_gate_kernel
+constexpr int kGateTokens = 2 * kThreads / 32;  // most tokens per CTA in metro_gate_kernel
 // auto policy of metro_route_scores_v1: above this many tokens the whole GPU takes
 // the top-k (measured crossover on B200: ~600 tokens at N = 256)
 constexpr int64_t kGateWholeGpuMin = 512;
@@ -914,12 +915,13 @@ __device__ __forceinline__ void lane_sort_desc(uint64_t (&c)[NPL]) {
 }
 
 // s_ids == nullptr: ids go to global memory only; hist[e * C + lane % C] counts.
-template <int NPL>
+// TPW: tokens in flight per warp (two at most for NPL <= 8: register budget).
+template <int NPL, int TPW = (NPL <= 8 ? 2 : 1)>
 __device__ void gate_topk(const Params &p, const Layout &L, unsigned char *smem, int64_t tok_beg, int n_tok,
                           int32_t *s_ids, int32_t *s_hist, int C) {
+    static_assert(TPW == 1 || (TPW == 2 && NPL <= 8), "register budget");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int N = p.N, k = p.top_k, cm = C - 1;
-    constexpr int TPW = NPL <= 8 ? 2 : 1;  // tokens in flight per warp (register budget)
     for (int t0 = TPW * warp; t0 < n_tok; t0 += TPW * kWarps) {
         const bool two = TPW == 2 && t0 + 1 < n_tok;
         uint64_t c[TPW][NPL];

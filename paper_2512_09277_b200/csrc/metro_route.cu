@@ -169,11 +169,15 @@ __global__ void __launch_bounds__(kThreads, 1) metro_gate_kernel(const Params p)
     int32_t &s_last = reinterpret_cast<int32_t *>(smem + L.misc)[63];  // misc is initialised later
     for (int e = tid; e < N; e += kThreads) s_hist[e] = 0;
     __syncthreads();
-    const int64_t tok_beg = static_cast<int64_t>(blockIdx.x) * kGateTokens;
+    const int64_t tok_beg = static_cast<int64_t>(blockIdx.x) * p.gate_tokens;
     const int64_t rem = p.num_tokens - tok_beg;
-    const int n_tok = rem <= 0 ? 0 : static_cast<int>(rem < kGateTokens ? rem : kGateTokens);
-    gate_topk<NPL>(p, L, smem, tok_beg, n_tok, nullptr, s_hist, 1);
+    const int n_tok = rem <= 0 ? 0 : static_cast<int>(rem < p.gate_tokens ? rem : p.gate_tokens);
+    uint64_t gt0 = 0, gt1 = 0, gt2 = 0;  // debug stamps (globaltimer) of this CTA
+    if (p.stamps && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
+    if (n_tok <= kWarps) gate_topk<NPL, 1>(p, L, smem, tok_beg, n_tok, nullptr, s_hist, 1);  // a token per warp
+    else gate_topk<NPL>(p, L, smem, tok_beg, n_tok, nullptr, s_hist, 1);
     __syncthreads();
+    if (p.stamps && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
     unsigned long long *wsT = reinterpret_cast<unsigned long long *>(p.gate_ws);
     for (int e = tid; e < N; e += kThreads)
         if (s_hist[e]) atomicAdd(wsT + e, static_cast<unsigned long long>(s_hist[e]));
@@ -188,6 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1) metro_gate_kernel(const Params p)
     __syncthreads();  // misc (s_last's home) is re-initialised below
     if (!last) return;
     __threadfence();  // every other CTA's ids and counts are visible from here on
+    if (p.stamps && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt2));
 
     // ---- last CTA: METRO from T (routing.py:105-113), then every pair's rank
     init_misc(reinterpret_cast<int32_t *>(smem + L.misc));
@@ -233,6 +238,14 @@ __global__ void __launch_bounds__(kThreads, 1) metro_gate_kernel(const Params p)
         p.status[0] = METRO_OK;
         p.status[1] = p.status[2] = 0;
         p.status[3] = static_cast<int32_t>(gridDim.x);
+        if (p.stamps) {  // the routing CTA's timeline (ns): start, top-k done, all arrived, end
+            uint64_t gt3;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt3));
+            p.stamps[20] = static_cast<int64_t>(gt0);
+            p.stamps[21] = static_cast<int64_t>(gt1);
+            p.stamps[22] = static_cast<int64_t>(gt2);
+            p.stamps[23] = static_cast<int64_t>(gt3);
+        }
     }
 }
 
@@ -767,7 +780,11 @@ int metro_route_scores_v1(const float *scores, int64_t num_tokens, int32_t top_k
     if (ws && (cluster_ctas < 0 || (cluster_ctas == 0 && num_tokens > kGateWholeGpuMin))) {
         // whole-GPU gating, last CTA routes
         p.gate_ws = ws;
-        const int64_t grid64 = (num_tokens + kGateTokens - 1) / kGateTokens;
+        // 32 tokens per CTA: spreading them thinner (2-16 per CTA, every SM busy) halves
+        // the top-k phase but the contended arrival/histogram atomics eat the gain
+        const int64_t tpc = kGateTokens;
+        p.gate_tokens = static_cast<int32_t>(tpc);
+        const int64_t grid64 = (num_tokens + tpc - 1) / tpc;
         const int grid = grid64 > 0 ? static_cast<int>(grid64) : 1;
         if (grid64 > INT32_MAX) return METRO_EDIMS;
         const int smem = make_layout(kMetroLoads, N, 1, 1, 0, 1, 0).total;
