@@ -113,13 +113,15 @@ METRO_API int metro_route_v1(const int32_t *topk_ids, int64_t num_pairs, const u
  * fp32 router scores of the all-gathered tokens; each token's top_k experts --
  * largest score first, ties to the lower expert id, the descending-key order of
  * the reference's generator (core.py:319-326) -- are written to topk_ids
- * [num_tokens, top_k] and routed in the same launch (no separate pass over the
- * ids).  Other outputs as metro_route_v1.
+ * [num_tokens, top_k] and counted as they are chosen (no separate pass over the
+ * ids), then routed.  Other outputs as metro_route_v1.
  * ws: metro_scores_workspace_bytes(N) bytes of device memory, ZEROED ONCE by the
  * caller; the kernel leaves it zeroed (one workspace per stream).  Two variants:
  *   whole GPU   -- 32 tokens' top-k per CTA on every SM, partial counts added into
- *                  ws with atomics, the last CTA to finish routes (needs ws);
- *   one cluster -- the routing cluster also takes the top-k (no ws needed).
+ *                  ws with atomics; a programmatically dependent launch of
+ *                  routing CTAs (resident while the top-k runs) routes from ws,
+ *                  each writing a share of the pair ranks (needs ws; two launches);
+ *   one cluster -- the routing cluster also takes the top-k (one launch, no ws).
  * cluster_ctas: 0 = auto (one cluster up to 512 tokens, whole GPU above when ws
  * is given), -1 = whole GPU, 1/2/4/8/16 = one cluster of that size.
  * Limits: N <= 512, G <= 32, top_k <= 32, top_k <= N; NaN scores are

@@ -51,10 +51,10 @@ struct Params {
     int32_t top_k;
     int32_t *ids_out;
     int32_t score_bytes;  // > 0: the CTA's score rows are staged in smem (bytes per CTA)
-    void *gate_ws;        // metro_gate_kernel: int64 T[N] + arrival counter, zero between launches
-    int32_t gate_tokens;  // metro_gate_kernel: tokens per CTA (<= kGateTokens)
+    void *gate_ws;        // whole-GPU gating: int64 T[N] + routing-CTA counter, zero between launches
+    int32_t gate_tokens;  // metro_gate_topk_kernel: tokens per CTA (<= kGateTokens)
 };
-constexpr int kGateTokens = 2 * kThreads / 32;  // most tokens per CTA in metro_gate_kernel
+constexpr int kGateTokens = 2 * kThreads / 32;  // tokens per CTA in metro_gate_topk_kernel
 // auto policy of metro_route_scores_v1: above this many tokens the whole GPU takes
 // the top-k (measured crossover on B200: ~600 tokens at N = 256)
 constexpr int64_t kGateWholeGpuMin = 512;

@@ -35,6 +35,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "../../include/metro_route.h"
@@ -148,97 +149,78 @@ __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) 
     stamp(p, 7);
 }
 
-// Gating top-k + METRO across the whole GPU in one launch (metro_route_scores_v1).
-// Every CTA takes top-k for 32 tokens (2 per warp), writes their ids and adds its
-// shared histogram into the int64 workspace T with global atomics; the last CTA
-// to finish (threadfence + arrival counter, no grid-wide barrier) routes from T
-// with the single-CTA decide path, writes every pair's rank, and re-zeroes the
-// workspace for the next launch.
-template <int W, int NPL>
-__global__ void __launch_bounds__(kThreads, 1) metro_gate_kernel(const Params p) {
-    griddep_wait();  // PDL launch: no global access before the previous kernel completes
-    griddep_launch_dependents();  // only once this kernel runs: at most one dependent waits
-    extern __shared__ __align__(128) unsigned char smem[];
-    const Layout L = make_layout(kMetroLoads, p.N, W, 1, 0, 1, 0);
+// The routing CTA(s) of the fused gating path: METRO from the workspace T
+// (routing.py:105-113), then the pair ranks of this CTA's share of the top-k
+// ids.  With several routing CTAs (split path) each decides redundantly (the
+// same deterministic result, no inter-CTA wait) and writes 1/parts of the pair
+// ranks; part 0 writes choice / counts / lambda / loads / status, and the last CTA
+// done reading T re-zeroes the workspace for the next launch.  Masks staged,
+// misc / aux free on entry.
+template <int W>
+__device__ void gate_route_tail(const Params &p, const Layout &L, unsigned char *smem, int32_t topk_ctas,
+                                uint64_t gt0, uint64_t gt1, uint64_t gt2, int part, int parts) {
     const int tid = threadIdx.x, N = p.N, k = p.top_k;
-    // every CTA stages the rank masks (1 KB) right away: whichever CTA ends up
-    // routing already has them
-    const StagePlan sp = stage_plan<W>(p, 0, 0, false);
-    if (tid == 0) stage_issue(p, L, smem, 0, sp);
-    int32_t *s_hist = reinterpret_cast<int32_t *>(smem + L.keys);  // decide scratch, free here
-    int32_t &s_last = reinterpret_cast<int32_t *>(smem + L.misc)[63];  // misc is initialised later
-    for (int e = tid; e < N; e += kThreads) s_hist[e] = 0;
-    __syncthreads();
-    const int64_t tok_beg = static_cast<int64_t>(blockIdx.x) * p.gate_tokens;
-    const int64_t rem = p.num_tokens - tok_beg;
-    const int n_tok = rem <= 0 ? 0 : static_cast<int>(rem < p.gate_tokens ? rem : p.gate_tokens);
-    uint64_t gt0 = 0, gt1 = 0, gt2 = 0;  // debug stamps (globaltimer) of this CTA
-    if (p.stamps && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
-    if (n_tok <= kWarps) gate_topk<NPL, 1>(p, L, smem, tok_beg, n_tok, nullptr, s_hist, 1);  // a token per warp
-    else gate_topk<NPL>(p, L, smem, tok_beg, n_tok, nullptr, s_hist, 1);
-    __syncthreads();
-    if (p.stamps && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
+    const bool writer = part == 0;
     unsigned long long *wsT = reinterpret_cast<unsigned long long *>(p.gate_ws);
-    for (int e = tid; e < N; e += kThreads)
-        if (s_hist[e]) atomicAdd(wsT + e, static_cast<unsigned long long>(s_hist[e]));
-    __threadfence();
-    __syncthreads();
-    unsigned int *arrived = reinterpret_cast<unsigned int *>(wsT + N);
-    if (tid == 0) s_last = (atomicAdd(arrived, 1u) == gridDim.x - 1);
-    stage_rest(p, L, smem, 0, 0, false, sp);
-    __syncthreads();
-    const bool last = s_last != 0;
-    mbar_wait(reinterpret_cast<uint64_t *>(smem + L.mbar), 0);  // no CTA exits with a copy in flight
-    __syncthreads();  // misc (s_last's home) is re-initialised below
-    if (!last) return;
-    __threadfence();  // every other CTA's ids and counts are visible from here on
-    if (p.stamps && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt2));
-
-    // ---- last CTA: METRO from T (routing.py:105-113), then every pair's rank
+    unsigned int *arrived = reinterpret_cast<unsigned int *>(wsT + N);  // routing CTAs done with T
+    int32_t &s_reset = reinterpret_cast<int32_t *>(smem + L.misc)[63];
     init_misc(reinterpret_cast<int32_t *>(smem + L.misc));
     zero_smem(smem, L.aux, L.hist);
+    if (tid == 0) s_reset = (parts == 1);
     __syncthreads();
     Params q = p;
     q.loads_in = reinterpret_cast<const int64_t *>(p.gate_ws);
-    const bool ok = metro_decide<W, kFromLoads>(q, L, smem, true, 1, 0);
+    const bool ok = metro_decide<W, kFromLoads>(q, L, smem, writer, 1, 0);
     __syncthreads();
-    for (int e = tid; e < N; e += kThreads) {  // loads out; workspace reset for the next launch
-        if (p.loads) p.loads[e] = static_cast<int32_t>(__ldcg(reinterpret_cast<const long long *>(wsT) + e));
-        wsT[e] = 0ull;
+    if (writer && p.loads)
+        for (int e = tid; e < N; e += kThreads)
+            p.loads[e] = static_cast<int32_t>(__ldcg(reinterpret_cast<const long long *>(wsT) + e));
+    if (parts > 1) {
+        __syncthreads();  // this CTA's reads of T are done
+        if (tid == 0 && atomicAdd(arrived, 1u) == static_cast<unsigned>(parts - 1)) s_reset = 1;
+        __syncthreads();
     }
-    if (tid == 0) *arrived = 0u;
+    if (s_reset) {  // workspace reset for the next launch (its top-k waits for this grid)
+        for (int e = tid; e < N; e += kThreads) wsT[e] = 0ull;
+        if (tid == 0) *arrived = 0u;
+    }
     if (!ok) return;
     const int32_t *s_choice = reinterpret_cast<const int32_t *>(smem + L.choice);
-    for (int e = tid; e < N; e += kThreads) p.choice[e] = s_choice[e];
+    if (writer)
+        for (int e = tid; e < N; e += kThreads) p.choice[e] = s_choice[e];
     if (p.pair_rank) {
-        // ids from L2 (written by the other CTAs): 16-byte loads, four in flight
+        // ids from L2 (written by the top-k CTAs): 16-byte loads, four in flight;
+        // this CTA's share [b4, e4) of the 16-byte groups
         const int64_t np = p.num_tokens * k;
         const int64_t n4 = ((reinterpret_cast<uintptr_t>(p.ids_out) | reinterpret_cast<uintptr_t>(p.pair_rank)) & 15)
                                ? 0 : (np >> 2);
+        const int64_t per = (n4 + parts - 1) / parts;
+        const int64_t b4 = min(n4, per * part), e4 = min(n4, b4 + per);
         const int4 *src4 = reinterpret_cast<const int4 *>(p.ids_out);
         int4 *dst4 = reinterpret_cast<int4 *>(p.pair_rank);
         constexpr int U = 4;
-        for (int64_t i0 = tid; i0 < n4; i0 += static_cast<int64_t>(kThreads) * U) {
+        for (int64_t i0 = b4 + tid; i0 < e4; i0 += static_cast<int64_t>(kThreads) * U) {
             int4 v[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int64_t i = i0 + static_cast<int64_t>(u) * kThreads;
-                v[u] = (i < n4) ? __ldcg(src4 + i) : make_int4(0, 0, 0, 0);
+                v[u] = (i < e4) ? __ldcg(src4 + i) : make_int4(0, 0, 0, 0);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int64_t i = i0 + static_cast<int64_t>(u) * kThreads;
-                if (i < n4)
+                if (i < e4)
                     dst4[i] = make_int4(s_choice[v[u].x], s_choice[v[u].y], s_choice[v[u].z], s_choice[v[u].w]);
             }
         }
-        for (int64_t i = n4 * 4 + tid; i < np; i += kThreads) p.pair_rank[i] = s_choice[__ldcg(p.ids_out + i)];
+        if (part == parts - 1)  // the scalar tail (unaligned buffers: everything)
+            for (int64_t i = n4 * 4 + tid; i < np; i += kThreads) p.pair_rank[i] = s_choice[__ldcg(p.ids_out + i)];
     }
-    if (tid == 0) {
+    if (writer && tid == 0) {
         p.status[0] = METRO_OK;
         p.status[1] = p.status[2] = 0;
-        p.status[3] = static_cast<int32_t>(gridDim.x);
-        if (p.stamps) {  // the routing CTA's timeline (ns): start, top-k done, all arrived, end
+        p.status[3] = topk_ctas;
+        if (p.stamps) {  // the routing CTA's timeline (ns)
             uint64_t gt3;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt3));
             p.stamps[20] = static_cast<int64_t>(gt0);
@@ -247,6 +229,67 @@ __global__ void __launch_bounds__(kThreads, 1) metro_gate_kernel(const Params p)
             p.stamps[23] = static_cast<int64_t>(gt3);
         }
     }
+}
+
+
+// Fused gating (metro_route_scores_v1, whole-GPU path), kernel 1 of 2: top-k of p.gate_tokens tokens per CTA, ids
+// out, CTA histogram added into the workspace T.  Its dependent (PDL) is
+// metro_gate_route_kernel, resident and waiting before this grid ends.
+template <int NPL>
+__global__ void __launch_bounds__(kThreads, 1) metro_gate_topk_kernel(const Params p) {
+    griddep_wait();  // the previous routing kernel may still be resetting the workspace
+    griddep_launch_dependents();
+    extern __shared__ __align__(128) unsigned char smem[];
+    const Layout L = make_layout(kMetroLoads, p.N, 1, 1, 0, 1, 0);
+    const int tid = threadIdx.x, N = p.N;
+    uint64_t t0 = 0;
+    if (p.stamps && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    int32_t *s_hist = reinterpret_cast<int32_t *>(smem);
+    for (int e = tid; e < N; e += kThreads) s_hist[e] = 0;
+    __syncthreads();
+    const int64_t tok_beg = static_cast<int64_t>(blockIdx.x) * p.gate_tokens;
+    const int64_t rem = p.num_tokens - tok_beg;
+    const int n_tok = rem <= 0 ? 0 : static_cast<int>(rem < p.gate_tokens ? rem : p.gate_tokens);
+    if (n_tok <= kWarps) gate_topk<NPL, 1>(p, L, smem, tok_beg, n_tok, nullptr, s_hist, 1);
+    else gate_topk<NPL>(p, L, smem, tok_beg, n_tok, nullptr, s_hist, 1);
+    __syncthreads();
+    unsigned long long *wsT = reinterpret_cast<unsigned long long *>(p.gate_ws);
+    for (int e = tid; e < N; e += kThreads)
+        if (s_hist[e]) atomicAdd(wsT + e, static_cast<unsigned long long>(s_hist[e]));
+    if (p.stamps && tid == 0) {  // debug: first CTA start, latest CTA end (globaltimer ns)
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMax(reinterpret_cast<unsigned long long *>(p.stamps + 25), static_cast<unsigned long long>(t));
+        if (blockIdx.x == 0) p.stamps[24] = static_cast<int64_t>(t0);
+    }
+}
+
+// Fused gating, kernel 2 of 2 (PDL dependent of the top-k grid): stages the
+// masks while the top-k runs, then routes once every top-k CTA is done.  A PDL
+// boundary (the dependent is resident and waiting) is cheaper than a
+// last-CTA-arrives handshake inside one kernel (fence + arrival atomics), and lets
+// several routing CTAs share the pair-rank pass.
+template <int W>
+__global__ void __launch_bounds__(kThreads, 1) metro_gate_route_kernel(const Params p) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const Layout L = make_layout(kMetroLoads, p.N, W, 1, 0, 1, 0);
+    const int tid = threadIdx.x;
+    uint64_t gt0 = 0;
+    if (p.stamps && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
+    // the masks are an input no kernel writes: staged before the dependency wait
+    const StagePlan sp = stage_plan<W>(p, 0, 0, false);
+    if (tid == 0) stage_issue(p, L, smem, 0, sp);
+    stage_rest(p, L, smem, 0, 0, false, sp);
+    mbar_wait(reinterpret_cast<uint64_t *>(smem + L.mbar), 0);
+    __syncthreads();
+    uint64_t gt1 = 0;
+    if (p.stamps && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
+    griddep_wait();  // every top-k CTA finished: ids and T complete and visible
+    griddep_launch_dependents();
+    uint64_t gt2 = 0;
+    if (p.stamps && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt2));
+    gate_route_tail<W>(p, L, smem, static_cast<int32_t>((p.num_tokens + p.gate_tokens - 1) / p.gate_tokens), gt0,
+                       gt1, gt2, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x));
 }
 
 // METRO from loads (compat route_metro(T, A)) or from a caller order (metro-parallel).
@@ -778,20 +821,26 @@ int metro_route_scores_v1(const float *scores, int64_t num_tokens, int32_t top_k
     p.pair_rank = pair_rank; p.status = status; p.stamps = g_stamps;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (ws && (cluster_ctas < 0 || (cluster_ctas == 0 && num_tokens > kGateWholeGpuMin))) {
-        // whole-GPU gating, last CTA routes
+        // whole-GPU gating: top-k grid, then routing CTAs (PDL)
         p.gate_ws = ws;
         // 32 tokens per CTA: spreading them thinner (2-16 per CTA, every SM busy) halves
         // the top-k phase but the contended arrival/histogram atomics eat the gain
-        const int64_t tpc = kGateTokens;
-        p.gate_tokens = static_cast<int32_t>(tpc);
-        const int64_t grid64 = (num_tokens + tpc - 1) / tpc;
+        // kernel 1: top-k, 32 tokens per CTA (spreading them thinner makes the
+        // contended histogram atomics cost more than the top-k saves)
+        p.gate_tokens = kGateTokens;
+        const int64_t grid64 = (num_tokens + kGateTokens - 1) / kGateTokens;
         const int grid = grid64 > 0 ? static_cast<int>(grid64) : 1;
         if (grid64 > INT32_MAX) return METRO_EDIMS;
-        const int smem = make_layout(kMetroLoads, N, 1, 1, 0, 1, 0).total;
+        const int smem1 = align_up(N * 4, 16);
         cudaError_t e;
-        if (N <= 128) e = launch_plain(metro_gate_kernel<1, 4>, grid, smem, s, p);
-        else if (N <= 256) e = launch_plain(metro_gate_kernel<1, 8>, grid, smem, s, p);
-        else e = launch_plain(metro_gate_kernel<1, 16>, grid, smem, s, p);
+        if (N <= 128) e = launch_plain(metro_gate_topk_kernel<4>, grid, smem1, s, p);
+        else if (N <= 256) e = launch_plain(metro_gate_topk_kernel<8>, grid, smem1, s, p);
+        else e = launch_plain(metro_gate_topk_kernel<16>, grid, smem1, s, p);
+        // kernel 2 (PDL dependent): routing CTAs, each deciding redundantly and
+        // writing ~512 pairs' ranks (measured: 16 CTAs at 8192-32768 pairs)
+        const int parts = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, (num_tokens * top_k + 511) / 512)));
+        const int smem = make_layout(kMetroLoads, N, 1, 1, 0, 1, 0).total;
+        if (e == cudaSuccess) e = launch_plain(metro_gate_route_kernel<1>, parts, smem, s, p);
         return e == cudaSuccess ? METRO_OK : cuda_fail(e);
     }
     int R = 1;

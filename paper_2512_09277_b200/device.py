@@ -197,9 +197,9 @@ class Router:
         ties to the lower expert id (the reference generator's order,
         core.py:319-326).
 
-        ``whole_gpu=True``: every SM takes top-k for 32 tokens and the last CTA
-        routes (a zeroed workspace owned by this Router; use one Router per
-        stream).  ``False``: the routing cluster also takes the top-k.  ``None``
+        ``whole_gpu=True``: every SM takes top-k for 32 tokens, then dependent
+        routing CTAs route from the summed counts (a zeroed workspace owned by
+        this Router; use one Router per stream).  ``False``: the routing cluster also takes the top-k.  ``None``
         (default): the library picks by batch size."""
         if self.kind != "metro":
             raise ValidationError("route_scores is the METRO router's fused gating entry point")

@@ -1,5 +1,6 @@
-"""Timeline of the whole-GPU fused gating kernel's routing CTA (globaltimer ns) and
-of the single-cluster variant (clock64 phases).  python tools/gate_phases.py"""
+"""Timeline of the whole-GPU fused gating path (globaltimer ns): top-k grid start /
+end, routing CTA 0 start, masks staged, PDL dependency released, end.
+python tools/gate_phases.py"""
 import ctypes
 import os
 import sys
@@ -27,8 +28,10 @@ def main():
         torch.cuda.synchronize()
         L.metro_debug_set_stamps(None)
         s = st.cpu().tolist()
-        print("whole-GPU B", B, "topk ns", s[21] - s[20], "arrival ns", s[22] - s[21], "route+outputs ns",
-              s[23] - s[22], "decide cycles", s[6] - s[3] if s[6] > s[3] else None, flush=True)
+        z = s[24]  # first top-k CTA's start
+        print("B", B, "ns after the top-k grid starts: grid done", s[25] - z, "routing CTA start", s[20] - z,
+              "masks staged", s[21] - z, "dependency released", s[22] - z, "end", s[23] - z, flush=True)
+        st.zero_()
 
 
 if __name__ == "__main__":
