@@ -895,8 +895,28 @@ __device__ __forceinline__ uint32_t okey(float f) {
 // that maximum) name the winner; its owner lane pops its head.  Ids are written in
 // descending score order (core.py:322-326), staged in shared memory for the
 // routing phases and counted into the lane-striped histogram.
+__device__ __forceinline__ void cas_desc(uint64_t &a, uint64_t &b) {
+    const uint64_t x = a, y = b;
+    const bool sw = x < y;
+    a = sw ? y : x;
+    b = sw ? x : y;
+}
 template <int NPL>
 __device__ __forceinline__ void lane_sort_desc(uint64_t (&c)[NPL]) {
+    if constexpr (NPL == 8) {
+        // optimal 8-input network: 19 compare-exchanges, depth 6 (bitonic: 24)
+        cas_desc(c[0], c[2]); cas_desc(c[1], c[3]); cas_desc(c[4], c[6]); cas_desc(c[5], c[7]);
+        cas_desc(c[0], c[4]); cas_desc(c[1], c[5]); cas_desc(c[2], c[6]); cas_desc(c[3], c[7]);
+        cas_desc(c[0], c[1]); cas_desc(c[2], c[3]); cas_desc(c[4], c[5]); cas_desc(c[6], c[7]);
+        cas_desc(c[2], c[4]); cas_desc(c[3], c[5]);
+        cas_desc(c[1], c[4]); cas_desc(c[3], c[6]);
+        cas_desc(c[1], c[2]); cas_desc(c[3], c[4]); cas_desc(c[5], c[6]);
+        return;
+    } else if constexpr (NPL == 4) {
+        cas_desc(c[0], c[1]); cas_desc(c[2], c[3]); cas_desc(c[0], c[2]); cas_desc(c[1], c[3]);
+        cas_desc(c[1], c[2]);
+        return;
+    }
 #pragma unroll
     for (int size = 2; size <= NPL; size <<= 1)
 #pragma unroll
