@@ -161,6 +161,25 @@ class Router:
             top_k=top_k,
         )
 
+    def _check_out(self, out: RouteResult, num_pairs: int) -> None:
+        """A caller-supplied result set must hold this launch's outputs (the kernel
+        writes through raw pointers): int32 on the placement's device, sized for
+        N experts, G ranks and ``num_pairs`` pair ranks."""
+        p = self.placement
+        need = [("loads", out.loads, p.num_experts), ("rank_counts", out.rank_counts, p.num_ranks),
+                ("lam", out.lam, 1), ("status", out.status, 4), ("pair_rank", out.pair_rank, num_pairs)]
+        if self.kind == "metro":
+            need.append(("choice", out.choice, p.num_experts))
+        else:
+            need.append(("x", out.x, p.num_experts * p.num_ranks))
+        for name, t, n in need:
+            if t is None:
+                if name in ("loads", "pair_rank", "x"):
+                    continue  # optional outputs
+                raise ValidationError(f"out.{name} is missing")
+            if t.dtype != torch.int32 or t.device != p.device or not t.is_contiguous() or t.numel() < n:
+                raise ValidationError(f"out.{name} must be a contiguous int32 tensor of >= {n} elements on {p.device}")
+
     def route(self, topk_ids: torch.Tensor, out: Optional[RouteResult] = None, pair_rank: bool = True,
               with_x: bool = False, stream: Optional[torch.cuda.Stream] = None) -> RouteResult:
         """Launch one routing kernel on ``stream`` (default: current stream)."""
@@ -169,6 +188,8 @@ class Router:
         num_pairs = ids.numel()
         if out is None:
             out = self.alloc(num_pairs, pair_rank=pair_rank, with_x=with_x, top_k=top_k)
+        else:
+            self._check_out(out, num_pairs)
         L = _native.lib()
         p = self.placement
         s = _stream(p.device, stream)
@@ -214,8 +235,13 @@ class Router:
         k = int(top_k)
         if topk_ids is None:
             topk_ids = torch.empty((B, k), dtype=torch.int32, device=p.device)
+        elif (topk_ids.dtype != torch.int32 or not topk_ids.is_cuda or topk_ids.device != p.device
+              or not topk_ids.is_contiguous() or topk_ids.numel() != B * k):
+            raise ValidationError(f"topk_ids must be a contiguous int32 tensor of {B}x{k} on {p.device}")
         if out is None:
             out = self.alloc(B * k, pair_rank=pair_rank, top_k=k)
+        else:
+            self._check_out(out, B * k)
         s = _stream(p.device, stream)
         ws = None
         cl = self.cluster_ctas

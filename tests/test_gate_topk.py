@@ -112,6 +112,34 @@ def test_fused_gate_limits_and_errors(_cuda):
         r.route_scores(torch.zeros((4, 256), device="cuda"), 33)  # k > 32
     with pytest.raises(ValidationError):
         r.route_scores(torch.zeros((4, 256), device="cuda", dtype=torch.float64), 8)
+    with pytest.raises(ValidationError):
+        r.route_scores(torch.zeros((4, 256), device="cuda"), 8,
+                       topk_ids=torch.empty((4, 8), dtype=torch.int64, device="cuda"))  # wrong dtype
+    with pytest.raises(ValidationError):
+        r.route_scores(torch.zeros((4, 256), device="cuda"), 8,
+                       topk_ids=torch.empty((4, 7), dtype=torch.int32, device="cuda"))  # wrong size
     big = DevicePlacement(np.ones((600, 8), np.int8))
     with pytest.raises(ValidationError):
         Router(big, "metro").route_scores(torch.zeros((4, 600), device="cuda"), 8)  # N > 512
+
+
+@pytest.mark.gpu
+def test_fused_gate_whole_gpu_sequence(_cuda):
+    """One router, consecutive whole-GPU launches of different sizes (1-16 routing
+    CTAs, pair counts not a multiple of 4): the workspace handoff between the
+    routing CTAs and the next launch's top-k grid, and an unaligned ids buffer."""
+    rng = np.random.default_rng(21)
+    A = make_placement(256, 8, 1.5, 7).matrix
+    r = Router(DevicePlacement(A), "metro")
+    for B in (1500, 3, 700, 4096, 65, 1, 2049):
+        sc = rng.standard_normal((B, 256)).astype(np.float32)
+        st = torch.from_numpy(sc).cuda()
+        if B == 65:  # topk_ids 4 bytes past a 16-byte boundary: scalar pair-rank path
+            buf = torch.empty(B * 6 + 1, dtype=torch.int32, device="cuda")
+            ids, out = r.route_scores(st, 6, topk_ids=buf[1:].view(B, 6), whole_gpu=True)
+        else:
+            ids, out = r.route_scores(st, 6, whole_gpu=True)
+        out.check()
+        got = ids.cpu().numpy()
+        assert (got == oracle.gate_topk(sc, 6)).all(), B
+        _check_routing(got, out, A)
