@@ -169,10 +169,10 @@ class ExchangeRoute:
         from . import _native
 
         ids = self.local if local_ids is None else local_ids
-        if ids.numel() != self.local_pairs or ids.dtype != torch.int32 or not ids.is_cuda:
-            raise ValueError("local_ids must be int32 CUDA [local_tokens, top_k]")
-        ids = ids.contiguous()
         p = self.placement
+        if ids.numel() != self.local_pairs or ids.dtype != torch.int32 or not ids.is_cuda or ids.device != p.device:
+            raise ValueError(f"local_ids must be int32 [local_tokens, top_k] on {p.device}")
+        ids = ids.contiguous()
         s = (stream if stream is not None else torch.cuda.current_stream(p.device)).cuda_stream
         o = self.out
         rc = self._fn(ids.data_ptr(), self.local_pairs, self.rank, self.world, self._peers, self.max_local_pairs,
