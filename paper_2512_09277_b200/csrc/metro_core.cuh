@@ -799,20 +799,20 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
                  ((Lp.hi + 0x01010101u) & 0x80808080u) == 0 &&
                  __dp4a(Lp.lo, 0x01010101u, __dp4a(Lp.hi, 0x01010101u, 0u)) == static_cast<uint32_t>(assigned);
             misc[M_PACKED_OK] = ok ? 1 : 0;
-            if (ok && writer) {
-                uint32_t mx = 0;
-                for (int g = 0; g < G; ++g) {
-                    const uint32_t c = ((g < 4 ? Lp.lo : Lp.hi) >> (8 * (g & 3))) & 0xffu;
-                    p.rank_counts[g] = static_cast<int32_t>(c);
-                    mx = max(mx, c);
-                }
-                *p.lam = static_cast<int32_t>(mx);
-            }
+            misc[M_PACKED_LO] = static_cast<int32_t>(Lp.lo);
+            misc[M_PACKED_HI] = static_cast<int32_t>(Lp.hi);
         }
         cta_sync();
         done = misc[M_PACKED_OK] != 0;
         if (done) {  // the greedy thread stored every choice as it went
             stamp(p, 6);
+            if (writer && warp == 0) {  // counts and lambda off the greedy thread's chain
+                const uint32_t w = static_cast<uint32_t>(misc[lane < 4 ? M_PACKED_LO : M_PACKED_HI]);
+                const uint32_t c = lane < G ? (w >> (8 * (lane & 3))) & 0xffu : 0u;
+                if (lane < G) p.rank_counts[lane] = static_cast<int32_t>(c);
+                const uint32_t mx = __reduce_max_sync(kFull, c);
+                if (lane == 0) *p.lam = static_cast<int32_t>(mx);
+            }
             return true;
         }
     }
