@@ -24,6 +24,7 @@ full metro metro_ids_kernel 5 python tools/profile_target.py metro
 full moe moe_gemm 0 python tools/k3_profile_target.py bf16 gate_up
 full moe_fp8 moe_gemm 0 python tools/k3_profile_target.py fp8 gate_up
 full moe_down moe_gemm 0 python tools/k3_profile_target.py bf16 down
+full moe_fp8_down moe_gemm 0 python tools/k3_profile_target.py fp8 down
 full gate metro_gate_topk_kernel 5 python tools/profile_target.py gate
 full gate_route metro_gate_route_kernel 5 python tools/profile_target.py gate
 full dispatch layout_kernel 5 python tools/profile_target.py dispatch

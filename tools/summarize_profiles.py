@@ -52,6 +52,7 @@ def main():
     traffic = {}
     for name, rep in (("metro", "metro_full.ncu-rep"), ("moe_gemm", "moe_full.ncu-rep"),
                       ("moe_gemm_fp8", "moe_fp8_full.ncu-rep"), ("moe_gemm_down", "moe_down_full.ncu-rep"),
+                      ("moe_gemm_fp8_down", "moe_fp8_down_full.ncu-rep"),
                       ("gate", "gate_full.ncu-rep"), ("gate_route", "gate_route_full.ncu-rep"),
                       ("dispatch", "dispatch_full.ncu-rep"),
                       ("exchange", "exchange_full.ncu-rep")):
