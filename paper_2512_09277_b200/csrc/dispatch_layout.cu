@@ -40,6 +40,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kMaxRep = 4096;
 constexpr int kMaxSlice = 8192;
+static_assert(kMaxSlice < 65536, "per-warp replica counts and prefixes are uint16");
 constexpr int kMaxCluster = 16;
 constexpr uint64_t kNoBad = ~0ull;
 
@@ -58,7 +59,7 @@ struct Params {
 };
 
 // smem: bad (8) | cta_tot [nrep + 1] | pre [nrep] | loc [nrep + 1] | off [nrep + 1] | sb [G + 1] | wsum [32] |
-//       hw [kWarps][nrep] | pk [slice] | rtab [N * G] (optional) | base [nrep] | e [slice] | g [slice]
+//       hw [kWarps][nrep] (uint16) | pk [slice] | rtab [N * G] (optional) | base [nrep] | e [slice] | g [slice]
 //       (pk = rid << 16 | in-warp rank; rtab = the replica table staged once;
 //        base[rid] = first row offset of rid's rank)
 struct Layout {
@@ -75,7 +76,7 @@ __host__ __device__ inline Layout make_layout(int nrep, int slice, int G, int rt
     L.off = o;  o = al16(o + (nrep + 1) * 4);
     L.sb = o;   o = al16(o + (G + 1) * 4);
     L.wsum = o; o = al16(o + 32 * 4);
-    L.hw = o;   o = al16(o + kWarps * nrep * 4);
+    L.hw = o;   o = al16(o + kWarps * nrep * 2);  // uint16: counts and prefixes <= kMaxSlice
     L.pk = o;   o = al16(o + slice * 4);
     L.rtab = o; o = al16(o + rtab_words * 4);
     L.base = o; o = al16(o + nrep * 4);
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, 1) layout_kernel(const Params p) {
     int32_t *s_off = reinterpret_cast<int32_t *>(smem + L.off);
     int32_t *s_sb = reinterpret_cast<int32_t *>(smem + L.sb);
     int32_t *s_wsum = reinterpret_cast<int32_t *>(smem + L.wsum);
-    int32_t *s_hw = reinterpret_cast<int32_t *>(smem + L.hw);
+    uint16_t *s_hw = reinterpret_cast<uint16_t *>(smem + L.hw);  // per-warp replica counts
     uint32_t *s_pk = reinterpret_cast<uint32_t *>(smem + L.pk);
     int32_t *s_rtab = reinterpret_cast<int32_t *>(smem + L.rtab);
     int32_t *s_base = reinterpret_cast<int32_t *>(smem + L.base);
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1) layout_kernel(const Params p) {
     // (1) warp sub-slices, match_any ranks
     const int ws = (((n_local + kWarps - 1) / kWarps) + 31) & ~31;
     const int wb = min(n_local, warp * ws), we = min(n_local, wb + ws);
-    int32_t *hw = s_hw + warp * nrep;
+    uint16_t *hw = s_hw + warp * nrep;
     unsigned long long my_bad = kNoBad;
     for (int p0 = wb; p0 < we; p0 += 32) {
         const int i = p0 + lane;
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1) layout_kernel(const Params p) {
             s_pk[i] = (static_cast<uint32_t>(rid) << 16) | static_cast<uint32_t>(r);
         }
         __syncwarp();
-        if (rid >= 0 && lane == __ffs(m) - 1) hw[rid] += __popc(m);
+        if (rid >= 0 && lane == __ffs(m) - 1) hw[rid] = static_cast<uint16_t>(hw[rid] + __popc(m));
         __syncwarp();
     }
     if (my_bad != kNoBad) atomicMin(s_bad, my_bad);
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1) layout_kernel(const Params p) {
 #pragma unroll 4
         for (int w = 0; w < kWarps; ++w) {
             const int32_t c = s_hw[w * nrep + rid];
-            s_hw[w * nrep + rid] = run;
+            s_hw[w * nrep + rid] = static_cast<uint16_t>(run);
             run += c;
         }
         s_tot[rid] = run;
