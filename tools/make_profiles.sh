@@ -26,7 +26,11 @@ full moe_fp8 moe_gemm 0 python tools/k3_profile_target.py fp8 gate_up
 full moe_down moe_gemm 0 python tools/k3_profile_target.py bf16 down
 full moe_fp8_down moe_gemm 0 python tools/k3_profile_target.py fp8 down
 full gate metro_gate_topk_kernel 5 python tools/profile_target.py gate
-full gate_route metro_gate_route_kernel 5 python tools/profile_target.py gate
+# the gating routing kernel (a PDL dependent that stages the masks before its wait) faults
+# under ncu's multi-pass KERNEL replay only (clean under compute-sanitizer memcheck /
+# racecheck, and in single-pass captures): application replay for this one
+$NCU --set full --import-source on --replay-mode application -k regex:metro_gate_route_kernel -s 5 -c 1 \
+    -o "$OUT/gate_route_full" python tools/profile_target.py gate > "$OUT/gate_route_full.log" 2>&1
 full dispatch layout_kernel 5 python tools/profile_target.py dispatch
 full exchange metro_allgather_kernel 5 python tools/profile_target.py exchange
 ls -la "$OUT"
