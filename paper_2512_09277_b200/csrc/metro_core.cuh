@@ -331,6 +331,10 @@ __device__ void histogram_push(const Params &p, const Layout &L, unsigned char *
             const int v = idx % nv;
             st_async_v4(row + 4 * v, d, reinterpret_cast<const uint4 *>(row)[v], xbar);
         }
+    } else {
+        // every thread's reads of the histogram counters are done before the decide
+        // phase writes its sort scratch over them (keys / cand alias hist)
+        cta_sync();
     }
     stamp(p, 18);
     if (R > 1) mbar_wait(xbar, 0);
