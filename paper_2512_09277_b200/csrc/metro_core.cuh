@@ -53,6 +53,7 @@ struct Params {
     int32_t score_bytes;  // > 0: the CTA's score rows are staged in smem (bytes per CTA)
     void *gate_ws;        // whole-GPU gating: int64 T[N] + routing-CTA counter, zero between launches
     int32_t gate_tokens;  // metro_gate_topk_kernel: tokens per CTA (<= kGateTokens)
+    int32_t private_scratch;  // one-CTA plan: the sort scratch has its own shared memory (no alias of hist)
 };
 constexpr int kGateTokens = 2 * kThreads / 32;  // tokens per CTA in metro_gate_topk_kernel
 // auto policy of metro_route_scores_v1: above this many tokens the whole GPU takes
@@ -79,7 +80,8 @@ __host__ __device__ inline int align_up(int x, int a) { return (x + a - 1) / a *
 constexpr int kES = 12;  // packed greedy entry stride (words)
 
 __host__ __device__ inline Layout make_layout(int kind, int N, int W, int R, int64_t slice,
-                                              int C, int staged, bool warp_hist = false, int score_bytes = 0) {
+                                              int C, int staged, bool warp_hist = false, int score_bytes = 0,
+                                              bool private_scratch = false) {
     Layout L;
     int o = 0;
     L.mbar = o; o += 16;
@@ -99,7 +101,10 @@ __host__ __device__ inline Layout make_layout(int kind, int N, int W, int R, int
     if (ids_mode) hist_bytes = warp_hist ? kWarps * N * 4 : N * C * 4;
     L.part = align_up(o + hist_bytes, 16);
     const int end1 = ids_mode ? align_up(L.part + R * L.NP * 4, 16) : L.part;
-    L.keys = o;
+    // the METRO sort scratch aliases hist + part (dead once T is reduced), unless the
+    // plan gives it its own space: then no barrier is needed between the last
+    // counter read and the first scratch write (one-CTA plans, histogram_push)
+    L.keys = (private_scratch && ids_mode && metro) ? end1 : o;
     L.cand = align_up(L.keys + (N + 16) * 8, 16);
     L.smask = L.cand;  // (unused: the warp greedy reads masks through sid)
     L.sid = align_up(L.cand + N * 4, 16);
@@ -331,7 +336,7 @@ __device__ void histogram_push(const Params &p, const Layout &L, unsigned char *
             const int v = idx % nv;
             st_async_v4(row + 4 * v, d, reinterpret_cast<const uint4 *>(row)[v], xbar);
         }
-    } else {
+    } else if (!p.private_scratch) {
         // every thread's reads of the histogram counters are done before the decide
         // phase writes its sort scratch over them (keys / cand alias hist)
         cta_sync();

@@ -49,7 +49,8 @@ template <int W, bool PRIV, int GATE_NPL = 0>
 __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t R = cluster_nctarank(), rank = cluster_ctarank();
-    const Layout L = make_layout(kMetroIds, p.N, W, R, p.slice, p.C, p.staged, PRIV, p.score_bytes);
+    const Layout L = make_layout(kMetroIds, p.N, W, R, p.slice, p.C, p.staged, PRIV, p.score_bytes,
+                                 p.private_scratch != 0);
     const int64_t beg = static_cast<int64_t>(rank) * p.slice;
     const int64_t rem_pairs = p.num_pairs - beg;
     const int n_local = rem_pairs <= 0 ? 0 : static_cast<int>(rem_pairs < p.slice ? rem_pairs : p.slice);
@@ -665,13 +666,18 @@ static int plan_ids(Kind kind, bool warp_hist, int64_t num_pairs, int N, int W, 
         if (slice > INT32_MAX / 8) continue;
         for (int staged = 1; staged >= 0; --staged) {
             for (int C = copies_for(N); C >= 1; C >>= 1) {
-                const Layout L = make_layout(kind, N, W, r, slice, C, staged, warp_hist);
-                if (L.total <= kMaxSmem) {
-                    p.slice = slice;
-                    p.staged = staged;
-                    p.C = C;
-                    R = r;
-                    return L.total;
+                // one CTA: prefer a sort scratch of its own (saves the barrier that
+                // orders the counter reads before the aliased scratch writes)
+                for (int priv = (r == 1 && kind == kMetroIds) ? 1 : 0; priv >= 0; --priv) {
+                    const Layout L = make_layout(kind, N, W, r, slice, C, staged, warp_hist, 0, priv != 0);
+                    if (L.total <= kMaxSmem) {
+                        p.slice = slice;
+                        p.staged = staged;
+                        p.C = C;
+                        p.private_scratch = priv;
+                        R = r;
+                        return L.total;
+                    }
                 }
                 if (warp_hist) break;  // C does not apply
             }
