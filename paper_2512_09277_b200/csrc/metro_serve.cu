@@ -126,7 +126,8 @@ __global__ void __launch_bounds__(kServeThreads, 1)
                        uint32_t stagger, int32_t *scratch) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31;
-    const Layout L = make_layout(kMetroIds, base.N, W, 1, base.slice, base.C, base.staged);
+    const Layout L = make_layout(kMetroIds, base.N, W, 1, base.slice, base.C, base.staged, false, 0,
+                                 base.private_scratch != 0);
     const bool staged = base.staged != 0;
     ServeReq &rq = *reinterpret_cast<ServeReq *>(smem + align_up(L.total, 16));
 
@@ -345,16 +346,18 @@ static int serve_plan(int N, int W, int64_t max_pairs, Params &p) {
     // pairs) the first pass also copies the ids to a device scratch buffer that
     // the pair-rank pass reads (HBM instead of a second PCIe read)
     for (int staged = 1; staged >= 0; --staged)
-        for (int C = C0; C >= 1; C >>= 1) {
-            const Layout L = make_layout(kMetroIds, N, W, 1, slice, C, staged);
-            const int total = align_up(L.total, 16) + static_cast<int>(sizeof(ServeReq));
-            if (total <= kMaxSmem) {
-                p.slice = slice;
-                p.staged = staged;
-                p.C = C;
-                return total;
+        for (int C = C0; C >= 1; C >>= 1)
+            for (int priv = 1; priv >= 0; --priv) {  // own sort scratch when it fits (no barrier)
+                const Layout L = make_layout(kMetroIds, N, W, 1, slice, C, staged, false, 0, priv != 0);
+                const int total = align_up(L.total, 16) + static_cast<int>(sizeof(ServeReq));
+                if (total <= kMaxSmem) {
+                    p.slice = slice;
+                    p.staged = staged;
+                    p.C = C;
+                    p.private_scratch = priv;
+                    return total;
+                }
             }
-        }
     return METRO_EDIMS;
 }
 
