@@ -124,8 +124,9 @@ METRO_API int metro_route_v1(const int32_t *topk_ids, int64_t num_pairs, const u
  *   one cluster -- the routing cluster also takes the top-k (one launch, no ws).
  * cluster_ctas: 0 = auto (one cluster up to 512 tokens, whole GPU above when ws
  * is given), -1 = whole GPU, 1/2/4/8/16 = one cluster of that size.
- * Limits: N <= 512, G <= 32, top_k <= 32, top_k <= N; NaN scores are
- * not supported. */
+ * Order: larger score first, equal scores (incl. -0.0 == +0.0) to the lower
+ * expert id, NaN below every number (taken last; ties among NaNs to the lower id).
+ * Limits: N <= 512, G <= 32, top_k <= 32, top_k <= N. */
 METRO_API size_t metro_scores_workspace_bytes(int32_t num_experts);
 METRO_API int metro_route_scores_v1(const float *scores, int64_t num_tokens, int32_t top_k,
                                     const uint32_t *rank_mask, int32_t num_experts, int32_t num_ranks,

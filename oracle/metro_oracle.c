@@ -40,6 +40,7 @@
  * Integer-only; no floating point anywhere on this path.
  */
 #include <stdint.h>
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -267,8 +268,11 @@ int oracle_dispatch_layout(const int32_t *ids, const int32_t *pair_rank, int64_t
     return rc;
 }
 
-/* Top-k of each token's scores, largest first; equal scores -> lower expert id.
- * Written as k rounds of "first maximum" over the not-yet-taken experts. */
+/* Top-k of each token's scores, largest first; equal scores -> lower expert id
+ * (-0.0 == +0.0 under float compare).  NaN ranks below every number (numpy's
+ * "NaN sorts last" in the reference generator's argsort(-keys), core.py:322-326),
+ * ties among NaNs -> lower id.  Written as k rounds of "first maximum" over the
+ * not-yet-taken experts. */
 void oracle_gate_topk(const float *scores, int64_t T, int32_t N, int32_t k, int32_t *ids) {
     unsigned char *taken = (unsigned char *)malloc((size_t)N + 1);
     for (int64_t t = 0; t < T; ++t) {
@@ -277,7 +281,8 @@ void oracle_gate_topk(const float *scores, int64_t T, int32_t N, int32_t k, int3
         for (int32_t r = 0; r < k; ++r) {
             int32_t best = -1;
             for (int32_t e = 0; e < N; ++e)
-                if (!taken[e] && (best < 0 || row[e] > row[best])) best = e;
+                if (!taken[e] && (best < 0 || (!isnan(row[e]) && (isnan(row[best]) || row[e] > row[best]))))
+                    best = e;
             taken[best] = 1;
             ids[t * k + r] = best;
         }

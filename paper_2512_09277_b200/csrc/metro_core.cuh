@@ -891,10 +891,16 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
 // ================================================================ kernels
 
 // ---------------------------------------------------------------- gating top-k (fused)
-// Order key of an fp32 score: unsigned compare == float compare (NaN excluded).
+// Order key of an fp32 score: unsigned compare == float compare.  -0.0 is
+// canonicalised to +0.0 (they compare equal, so the tie goes to the lower id, as
+// the oracle's float '>' does), and every NaN maps to 0, below every number
+// (-inf keys to 0x007fffff): NaN scores are taken last, ties among them to the
+// lower id -- numpy's "NaN sorts last" in the reference generator's argsort(-keys)
+// (core.py:322-326).  A key of 0 still beats the padding lanes (whole key 0).
 __device__ __forceinline__ uint32_t okey(float f) {
-    const uint32_t b = __float_as_uint(f);
-    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    const uint32_t b = (f == 0.0f) ? 0u : __float_as_uint(f);
+    const uint32_t k = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    return (f != f) ? 0u : k;
 }
 // Top-k of every token of this CTA's slice, fused with the histogram: one warp per
 // token, two tokens in flight per warp (one for N > 256).  Lane l holds experts l + 32 j as 64-bit

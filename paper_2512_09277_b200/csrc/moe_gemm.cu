@@ -60,10 +60,14 @@ struct Item {
 // loads the NEXT item while it works on the current one, so no role starts an
 // item with a descriptor round trip on its critical path (~1 % on the FP8 down
 // projection, whose 2016 items carry 16 k-blocks each).
-__device__ __forceinline__ Item load_item(const Item *items, int it, int n_items) {
+// Memory-safety guard: a token count outside [0, max_n] (the tiling's B stage and
+// TMEM accumulator width) is clamped, so a malformed item can never overrun shared
+// memory or TMEM.  Host items are checked before launch (moe.py); device items
+// from moe_layout_items_v1 respect the bound by construction.
+__device__ __forceinline__ Item load_item(const Item *items, int it, int n_items, int max_n) {
     if (it >= n_items) return Item{0, 0, 0, 0};
     const int4 v = __ldg(reinterpret_cast<const int4 *>(items + it));
-    return Item{v.x, v.y, v.z, v.w};
+    return Item{v.x, v.y, v.z, min(max(v.w, 0), max_n)};
 }
 
 struct Params {
@@ -231,10 +235,10 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            Item nxt = load_item(p.items, blockIdx.x, n_items);
+            Item nxt = load_item(p.items, blockIdx.x, n_items, TL::kN);
             for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
                 const Item item = nxt;
-                nxt = load_item(p.items, it + gridDim.x, n_items);
+                nxt = load_item(p.items, it + gridDim.x, n_items, TL::kN);
                 const int mi = map_index(item.n);
                 const uint32_t bbytes = static_cast<uint32_t>((16 << mi) * BK * 2);
                 for (int kb = 0; kb < kblocks; ++kb) {
@@ -255,10 +259,10 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
-            Item nxt = load_item(p.items, blockIdx.x, n_items);
+            Item nxt = load_item(p.items, blockIdx.x, n_items, TL::kN);
             for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
                 const Item item = nxt;
-                nxt = load_item(p.items, it + gridDim.x, n_items);
+                nxt = load_item(p.items, it + gridDim.x, n_items, TL::kN);
                 const int acc = local & 1;
                 const uint32_t aphase = (local >> 1) & 1;
                 mbar_wait(&tempty[acc], aphase ^ 1);
@@ -291,10 +295,10 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     } else {
         // ---------------- epilogue: warps 0-3 own TMEM lanes 32w .. 32w+31 (= W rows)
         int local = 0;
-        Item nxt = load_item(p.items, blockIdx.x, n_items);
+        Item nxt = load_item(p.items, blockIdx.x, n_items, TL::kN);
         for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++local) {
             const Item item = nxt;
-            nxt = load_item(p.items, it + gridDim.x, n_items);
+            nxt = load_item(p.items, it + gridDim.x, n_items, TL::kN);
             const int acc = local & 1;
             const uint32_t aphase = (local >> 1) & 1;
             mbar_wait(&tfull[acc], aphase);

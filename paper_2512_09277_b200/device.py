@@ -319,6 +319,8 @@ class HostRouter:
 
     def run(self, num_pairs: int) -> np.ndarray:
         """Route ids[:num_pairs] (already written into self.ids); synchronous."""
+        if not 0 <= num_pairs <= self.max_pairs:
+            raise ValidationError("batch larger than the HostRouter workspace")
         self._npairs.value = num_pairs
         rc = self._fn(*self._args)
         if rc:

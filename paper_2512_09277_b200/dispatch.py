@@ -94,6 +94,13 @@ class DispatchLayout:
                 status=torch.empty(4, dtype=torch.int32, device=pl.device),
                 top_k=topk_ids.shape[-1] if topk_ids.dim() == 2 else 1,
             )
+        else:  # the kernel writes through raw pointers: a caller's buffers must fit
+            for name, t, n in (("pair_row", out.pair_row, P), ("rep_off", out.rep_off, self.nrep + 1),
+                               ("status", out.status, 4)):
+                if (not isinstance(t, torch.Tensor) or t.dtype != torch.int32 or t.device != pl.device
+                        or not t.is_contiguous() or t.numel() < n):
+                    raise ValidationError(f"out.{name} must be a contiguous int32 tensor of >= {n} elements "
+                                          f"on {pl.device}")
         s = stream if stream is not None else torch.cuda.current_stream(pl.device)
         rc = _native.lib().metro_dispatch_layout_v1(
             ids.data_ptr() if P else None, pr.data_ptr() if P else None, P,

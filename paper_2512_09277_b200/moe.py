@@ -91,6 +91,23 @@ def build_items(groups: Sequence[Tuple[int, int, int]], M: int) -> np.ndarray:
     return np.asarray(out, dtype=np.int32).reshape(-1, 4)
 
 
+def _items_and_bound(items, max_item_tokens):
+    """(items as a tensor, token bound).  Host items: the bound is their largest
+    token count, and an explicit bound below it is rejected (a bound <= item_tokens()
+    selects the 64-token tiling).  Device items are not read back: without an
+    explicit bound the wide tiling (any count <= 256) runs, and the kernel clamps
+    every count to its tiling as a memory-safety guard (moe_gemm.cu load_item)."""
+    if isinstance(items, torch.Tensor) and items.is_cuda:
+        return items, (MAXN if max_item_tokens is None else int(max_item_tokens))
+    a = np.asarray(items.cpu() if isinstance(items, torch.Tensor) else items).reshape(-1, 4)
+    most = int(a[:, 3].max()) if len(a) else 1
+    if max_item_tokens is None:
+        max_item_tokens = most
+    elif most > int(max_item_tokens):
+        raise ValidationError(f"an item has {most} tokens, above max_item_tokens={int(max_item_tokens)}")
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)), int(max_item_tokens)
+
+
 def grouped_gemm(W: torch.Tensor, X: torch.Tensor, items, Y: torch.Tensor = None,
                  num_ctas: int = 0, max_item_tokens: int = None) -> torch.Tensor:
     """Y[t, m] = sum_k W[e][m, k] X[t, k] for every item (bf16 in/out, fp32 accumulate).
@@ -98,13 +115,7 @@ def grouped_gemm(W: torch.Tensor, X: torch.Tensor, items, Y: torch.Tensor = None
     ``max_item_tokens`` bounds the items' token counts: <= item_tokens() selects
     the deeper-pipelined narrow tiling.  Taken from host items; device items
     without it use the wide tiling (any count <= 256)."""
-    if max_item_tokens is None:
-        if isinstance(items, np.ndarray) or (isinstance(items, torch.Tensor) and not items.is_cuda):
-            a = np.asarray(items).reshape(-1, 4)
-            max_item_tokens = int(a[:, 3].max()) if len(a) else 1
-        else:
-            max_item_tokens = MAXN
-        items = torch.as_tensor(np.asarray(items).reshape(-1, 4) if isinstance(items, np.ndarray) else items)
+    items, max_item_tokens = _items_and_bound(items, max_item_tokens)
     if W.dtype != torch.bfloat16 or X.dtype != torch.bfloat16:
         raise ValidationError("W and X must be bfloat16")
     if W.dim() != 3 or X.dim() != 2 or W.shape[2] != X.shape[1]:
@@ -220,13 +231,7 @@ def grouped_gemm_fp8(W8: torch.Tensor, w_scale: torch.Tensor, X8: torch.Tensor, 
         raise ValidationError("W8 and X8 must be E4M3 bytes (uint8)")
     E, M, K = W8.shape
     T = X8.shape[0]
-    if max_item_tokens is None:
-        if isinstance(items, np.ndarray) or (isinstance(items, torch.Tensor) and not items.is_cuda):
-            a = np.asarray(items).reshape(-1, 4)
-            max_item_tokens = int(a[:, 3].max()) if len(a) else 1
-        else:
-            max_item_tokens = MAXN
-    items = torch.as_tensor(np.asarray(items).reshape(-1, 4) if isinstance(items, np.ndarray) else items)
+    items, max_item_tokens = _items_and_bound(items, max_item_tokens)
     items = items.to(device=W8.device, dtype=torch.int32).contiguous()
     if Y is None:
         Y = torch.empty((T, M), dtype=torch.bfloat16, device=W8.device)

@@ -9,7 +9,8 @@ from paper_2512_09277_b200 import routing
 
 def test_reference_names_exported(eproute_ref):
     missing = [n for n in eproute_ref.__all__ if not hasattr(pkg, n)]
-    # trace JSONL IO and the cost model are outside the routing hot path
+    # the cost model (CostProfile / LayerTiming) is outside the routing hot path;
+    # the trace / placement JSONL IO is built (io.py)
     allowed = {"CostProfile", "LayerTiming"}
     assert set(missing) <= allowed, missing
 
@@ -74,3 +75,17 @@ def test_token_batch_roundtrip():
     assert [t.source_gpu for t in b.tokens] == [0, 1, 0]
     assert np.array_equal(b.topk_ids(2), ids)
     assert b.max_tokens_per_source_gpu(2) == 2
+
+
+def test_moe_item_bound_checked_on_host():
+    """an explicit max_item_tokens below a host item's token count is
+    rejected before launch (it would select the 64-token tiling); numpy items with
+    an explicit bound are converted (no AttributeError)."""
+    from paper_2512_09277_b200 import moe
+    items = np.array([[0, 0, 0, 100], [1, 0, 100, 30]], np.int32)
+    t, bound = moe._items_and_bound(items, None)
+    assert bound == 100 and tuple(t.shape) == (2, 4)
+    t, bound = moe._items_and_bound(items, 256)
+    assert bound == 256 and t.dtype == __import__("torch").int32
+    with pytest.raises(pkg.ValidationError, match="above max_item_tokens"):
+        moe._items_and_bound(items, 64)

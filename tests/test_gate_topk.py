@@ -26,6 +26,28 @@ def test_oracle_topk_ties_lower_id():
     assert oracle.gate_topk(sc, 4).tolist() == [[1, 2, 4, 3]]
 
 
+def test_oracle_topk_signed_zero_and_nan():
+    nan = np.float32("nan")
+    # -0.0 == +0.0: the lower id wins; NaN ranks below every number, even -inf
+    sc = np.array([[-0.0, 0.0, -1.0],
+                   [0.0, -0.0, -1.0],
+                   [nan, -np.inf, 1.0],
+                   [nan, nan, -0.0]], np.float32)
+    assert oracle.gate_topk(sc, 3).tolist() == [[0, 1, 2], [0, 1, 2], [2, 1, 0], [2, 0, 1]]
+    assert oracle.gate_topk(sc, 1).tolist() == [[0], [0], [2], [2]]
+
+
+def _signed_zero_nan_scores(rng, B, n):
+    """Rows that stress the key order: +-0.0 mixes, NaNs and +-inf among a few
+    distinct values, so the k-th boundary often falls inside a tie class."""
+    vals = np.array([-0.0, 0.0, -0.0, 0.0, 1.0, -1.0, np.inf, -np.inf, np.nan, 0.5], np.float32)
+    sc = vals[rng.integers(0, len(vals), size=(B, n))]
+    # a quarter of the rows: all zeros of random sign (k = 1 picks the lowest id)
+    z = rng.random(B) < 0.25
+    sc[z] = np.where(rng.random((int(z.sum()), n)) < 0.5, np.float32(-0.0), np.float32(0.0))
+    return sc
+
+
 @pytest.fixture(scope="module")
 def _cuda():
     if not torch.cuda.is_available():
@@ -143,3 +165,23 @@ def test_fused_gate_whole_gpu_sequence(_cuda):
         got = ids.cpu().numpy()
         assert (got == oracle.gate_topk(sc, 6)).all(), B
         _check_routing(got, out, A)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["gpu", 1, 4])
+def test_fused_gate_signed_zero_and_nan(_cuda, variant):
+    """Bit-exact ids vs the oracle on +-0.0 / NaN / +-inf rows, k = 1 and k at a
+    tie boundary, both gating variants (whole GPU and one cluster)."""
+    rng = np.random.default_rng(77)
+    for n, g in ((256, 8), (128, 8), (64, 4), (300, 16)):
+        A = make_placement(n, g, 1.5, 7).matrix
+        for k in (1, 2, 8):
+            for B in (1, 37, 700):
+                sc = _signed_zero_nan_scores(rng, B, n)
+                if variant == "gpu":
+                    ids, out = _fused(sc, k, A, whole_gpu=True)
+                else:
+                    ids, out = _fused(sc, k, A, variant, whole_gpu=False)
+                ref = oracle.gate_topk(sc, k)
+                assert (ids == ref).all(), (n, k, B, variant)
+                _check_routing(ids, out, A)

@@ -109,7 +109,14 @@ def check_gate(rng, A):
         return {}
     k = int(rng.integers(1, min(32, n) + 1))
     B = int(rng.choice([1, 31, 256, 513, 1024, 2049]))
-    sc = (rng.integers(-3, 4, size=(B, n)) if rng.random() < 0.3 else rng.standard_normal((B, n))).astype(np.float32)
+    u = rng.random()
+    if u < 0.25:  # heavy ties: small integers
+        sc = rng.integers(-3, 4, size=(B, n)).astype(np.float32)
+    elif u < 0.45:  # signed zeros, NaN, +-inf among a few values (key-order edge cases)
+        vals = np.array([-0.0, 0.0, -0.0, 0.0, 1.0, -1.0, np.inf, -np.inf, np.nan, 0.5], np.float32)
+        sc = vals[rng.integers(0, len(vals), size=(B, n))]
+    else:
+        sc = rng.standard_normal((B, n)).astype(np.float32)
     r = Router(DevicePlacement(A), "metro", int(rng.choice([0, 1, 4, 16])))
     whole = [None, True, False][int(rng.integers(3))]
     ids, o = r.route_scores(torch.from_numpy(sc).cuda(), k, whole_gpu=whole)
