@@ -173,7 +173,7 @@ def test_fused_gate_signed_zero_and_nan(_cuda, variant):
     """Bit-exact ids vs the oracle on +-0.0 / NaN / +-inf rows, k = 1 and k at a
     tie boundary, both gating variants (whole GPU and one cluster)."""
     rng = np.random.default_rng(77)
-    for n, g in ((256, 8), (128, 8), (64, 4), (300, 16)):
+    for n, g in ((256, 8), (128, 8), (64, 4), (320, 16)):
         A = make_placement(n, g, 1.5, 7).matrix
         for k in (1, 2, 8):
             for B in (1, 37, 700):
