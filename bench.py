@@ -168,22 +168,49 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU (oracle port)
-def cpu_route_layers(A, batches, seconds: float, min_layers: int = 0):
-    """Time the oracle port (aggregate_loads + route_metro + pair_rank) per layer on
-    one host core; returns (µs/layer, layers, outputs of the first len(batches))."""
+class OneCore:
+    """Pin the calling thread to one host core (the last of its affinity set) for
+    a single-thread CPU timing, restoring the affinity afterwards."""
+
+    def __enter__(self):
+        self.saved = os.sched_getaffinity(0)
+        self.core = max(self.saved)
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *a):
+        os.sched_setaffinity(0, self.saved)
+
+
+def cpu_layer_sample(A, batches, seconds: float, min_layers: int = 200):
+    """The oracle port's layer (aggregate_loads + route_metro + pair_rank) timed
+    one layer at a time (perf_counter around each call) on ONE pinned host core,
+    cycling through the batches, for at least `seconds` and `min_layers` layers.
+    Returns (per-layer µs list, outputs of the batches for the parity check).
+    Both arms use this one function: the reference arm and the b200 arm's
+    cpu_baseline leg measure the same thing the same way."""
     import oracle
 
     outs = [oracle.metro_layer(b, A) for b in batches]  # warm + results for the parity check
     scratch = [tuple(np.copy(x) for x in o) for o in outs]
-    n, t0 = 0, time.perf_counter()
-    while True:
-        for i, b in enumerate(batches):
-            oracle.metro_layer(b, A, scratch[i])
-        n += len(batches)
-        el = time.perf_counter() - t0
-        if el >= seconds and n >= min_layers:
-            break
-    return el / n * 1e6, n, outs
+    per = []
+    t_end = time.perf_counter() + seconds
+    i = 0
+    with OneCore():
+        while True:
+            b = batches[i % len(batches)]
+            t0 = time.perf_counter()
+            oracle.metro_layer(b, A, scratch[i % len(batches)])
+            per.append(time.perf_counter() - t0)
+            i += 1
+            if len(per) >= min_layers and (i % len(batches) == 0) and time.perf_counter() >= t_end:
+                break
+    return [x * 1e6 for x in per], outs
+
+
+def stats_us(per):
+    s = sorted(per)
+    return {"mean": statistics.mean(s), "median": s[len(s) // 2], "p99": s[int(len(s) * 0.99)], "layers": len(s)}
 
 
 def cpu_model() -> str:
@@ -249,35 +276,41 @@ def cpu_allcores_throughput(A, batches, seconds: float = 2.0):
 
 
 def run_reference(args, cfg, rank: int, world: int):
+    """The reference algorithm's CPU path (the oracle port) on one pinned host
+    core, on this arm's workload.  A step is a bounded sample of layers sized so
+    the whole timed run covers >= 1 s and >= 200 layers whatever --steps is;
+    value = mean µs per layer over every timed layer (median / p99 beside it)."""
     if rank != 0:
         return None
     A, batches = workload(cfg, world)
     import oracle
 
     oracle.build()
+    steps = max(1, args.steps)
+    # calibrate: layers per step so that steps x per_step >= max(200 layers, 1 s)
+    cal, _ = cpu_layer_sample(A, batches, 0.2, 64)
+    target = max(200, int(1.0 / (statistics.mean(cal) * 1e-6)) + 1)
+    per_step = -(-max(1, -(-target // steps)) // len(batches)) * len(batches)  # whole passes over the pool
     for _ in range(args.warmup):
-        for b in batches[:4]:
-            oracle.metro_layer(b, A)
-    # each step: one layer = one batch of the same workload, on one host core
+        cpu_layer_sample(A, batches, 0.0, min(per_step, 64))
     per = []
-    scratch = [oracle.metro_layer(b, A) for b in batches]
-    for s in range(args.steps):
-        b = batches[s % len(batches)]
-        t0 = time.perf_counter()
-        oracle.metro_layer(b, A, scratch[s % len(batches)])
-        per.append(time.perf_counter() - t0)
-    us = statistics.mean(per) * 1e6
+    for _ in range(steps):
+        p, _ = cpu_layer_sample(A, batches, 0.0, per_step)
+        per.extend(p)
+    st = stats_us(per)
+    us = st["mean"]
     thr, cores = cpu_allcores_throughput(A, batches, 1.0)
-    sample = (f"{args.steps} layers of the {args.config} workload (B={cfg['B']}, N={cfg['N']}, "
-              f"G={cfg['G']}), one layer per step, single thread")
+    sample = (f"{st['layers']} layers of the {args.config} workload (B={cfg['B']}, N={cfg['N']}, G={cfg['G']}): "
+              f"{steps} steps of {per_step} layers, each layer timed alone, one pinned host core")
     return {
         "impl": "reference", "metric": METRIC, "value": us, "unit": "us/layer", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": us * per_step / 1e3, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": data_str(cfg),
-        "config": dict(config_dict(args, cfg, world), l2="n/a (host CPU path)",
-                       parallelism="single host thread, one layer per step"),
+        "config": config_dict(args, cfg, world),
+        "arm": "reference algorithm's CPU path: the oracle port (oracle/metro_oracle.c), single thread, pinned",
         "cpu_baseline": {"value": us, "unit": "us/layer", "cores": 1, "kind": "port", "sample": sample,
-                         "all_cores_layers_per_s": thr, "host_cores": cores, "cpu_model": cpu_model()},
+                         "per_layer_us": st, "all_cores_layers_per_s": thr, "host_cores": cores,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": us, "unit": "us/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -289,10 +322,13 @@ def data_str(cfg=None):
 
 
 def config_dict(args, cfg, world):
+    """The workload, identical in both arms (the driver compares the two lines'
+    config); how each arm runs it is under the line's "arm" / "timing" keys."""
     return {"workload": cfg["workload"], "name": args.config, "num_experts": cfg["N"], "top_k": cfg["k"],
             "ep_ranks": cfg["G"], "replication": cfg["ratio"], "global_batch": cfg["B"],
             "parallelism": f"ep all-gather over {world} GPU(s), routing replicated per rank",
-            "l2": "flushed between steps (256 MiB memset outside the timed events)",
+            "l2": ("inputs larger than L2 (256 MiB pool cycled, no flush)" if world == 1 else
+                   "flushed between steps (256 MiB memset, subtracted)"),
             "pool_batches": POOL}
 
 
@@ -600,6 +636,7 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "int32", "data": data_str(cfg),
         "config": config_dict(args, cfg, world),
+        "arm": "b200: sm_100a routing kernels (libmetro_b200.so) through the C ABI",
         "e2e": dict({"value": e2e_us, "unit": "us/layer", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
                     **e2e_extra),
         "gpu_launches": K_eff,
@@ -614,8 +651,6 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
                    "metro_le_eplb_all": all(a <= b for a, b in zip(lam_m, lam_e)), "batches": len(lam_m)},
         "clocks": clk.summary(),
     }
-    res["config"]["l2"] = ("inputs larger than L2 (256 MiB pool cycled, no flush)" if world == 1 else
-                           "flushed between steps (256 MiB memset, subtracted)")
     if world > 1:
         recv = (world - 1) * lt * k * 4
         res["nvlink"] = {"allgather_recv_bytes_per_rank": recv,
@@ -653,8 +688,10 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
             "routing_share_of_metro_layer": step_ms * 1e3 / m8["metro"]["device_layer_us"],
         }
     if world == 1:
-        us, layers, outs = cpu_route_layers(A, batches, args.cpu_seconds)
-        parity = all(int(o[3][0]) == lm for o, lm in zip(outs, lam_m))
+        per, outs = cpu_layer_sample(A, batches, args.cpu_seconds)
+        st = stats_us(per)
+        lam_cpu = [int(o[3][0]) for o in outs]
+        parity = lam_cpu == lam_m[:len(lam_cpu)]
         # full-output parity of the last exact batch (choice / pair_rank)
         router.route(base[-1], out=out)
         torch.cuda.synchronize()
@@ -663,11 +700,12 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
             np.array_equal(out.pair_rank.cpu().numpy(), o[4].reshape(-1))
         thr, cores = cpu_allcores_throughput(A, batches, 1.0)
         res["cpu_baseline"] = {
-            "value": us, "unit": "us/layer", "cores": 1, "kind": "port",
-            "sample": f"{layers} layers ({args.cpu_seconds:.0f} s) of this workload through the oracle "
-                      "port (aggregate_loads + route_metro + pair_rank), single thread",
-            "all_cores_layers_per_s": thr, "host_cores": cores, "cpu_model": cpu_model(),
-            "per_layer": cpu_per_layer_stats(A, batches), "parity_vs_gpu": bool(parity),
+            "value": st["mean"], "unit": "us/layer", "cores": 1, "kind": "port",
+            "sample": f"{st['layers']} layers ({args.cpu_seconds:.0f} s) of this workload through the oracle "
+                      "port (aggregate_loads + route_metro + pair_rank), each layer timed alone, one pinned "
+                      "host core (the same function as --impl reference)",
+            "per_layer_us": st, "all_cores_layers_per_s": thr, "host_cores": cores, "cpu_model": cpu_model(),
+            "eplb_layer_us": cpu_per_layer_stats(A, batches)["eplb_layer_us"], "parity_vs_gpu": bool(parity),
         }
     return res
 

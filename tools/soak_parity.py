@@ -180,15 +180,12 @@ def check_exchange(rng, ids, A, pl):
             b.close()
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--seconds", type=float, default=600)
-    ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--out", default="gpurun_out/soak.json")
-    a = ap.parse_args()
-    rng = np.random.default_rng(a.seed)
+def run(seconds: float, seed: int = 1) -> dict:
+    """Random instances through every device entry point for `seconds`; returns
+    the tally (instances, per-check run / mismatch counts, failures)."""
+    rng = np.random.default_rng(seed)
     tally, fails, skipped = {}, [], {}
-    t_end = time.time() + a.seconds
+    t_end = time.time() + seconds
     it = 0
     while time.time() < t_end:
         it += 1
@@ -225,10 +222,20 @@ def main():
             c[1] += 0 if ok else 1
             if not ok and len(fails) < 20 and key != "exception":
                 fails.append({"iter": it, "check": key, "N": A.shape[0], "G": A.shape[1], "shape": list(ids.shape)})
-    summary = {"seconds": a.seconds, "seed": a.seed, "instances": it,
-               "checks": {k: {"run": v[0], "mismatches": v[1]} for k, v in sorted(tally.items())},
-               "skipped_outside_documented_limits": skipped,
-               "failures": fails}
+    return {"seconds": seconds, "seed": seed, "instances": it,
+            "checks": {k: {"run": v[0], "mismatches": v[1]} for k, v in sorted(tally.items())},
+            "skipped_outside_documented_limits": skipped,
+            "failures": fails}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--seconds", type=float, default=600)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--out", default="gpurun_out/soak.json")
+    a = ap.parse_args()
+    summary = run(a.seconds, a.seed)
+    fails = summary["failures"]
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out, "w") as f:
         json.dump(summary, f, indent=1)
