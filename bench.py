@@ -481,8 +481,28 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
             single.sort()
             method["single_launch_us"] = {"mean": statistics.mean(single), "p50": single[len(single) // 2],
                                           "p99": single[int(len(single) * 0.99)], "samples": len(single),
-                                          "note": "events around one eager launch on an idle stream: includes "
-                                                  "the host launch path (Python, ctypes, driver)"}
+                                          "note": "events around one eager Router.route launch on an idle "
+                                                  "stream: includes the host launch path (Python, ctypes, "
+                                                  "driver)"}
+            # the lean eager path: a launch plan bound to fixed buffers (Router.bind,
+            # metro_route_plan_launch_v1), the ids refilled in place each layer
+            slot = base[0].clone()
+            plan = router.bind(slot, out=out)
+            single = []
+            for i in range(500):
+                slot.copy_(base[i % POOL])
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record()
+                plan()
+                e1.record()
+                torch.cuda.synchronize()
+                single.append(e0.elapsed_time(e1) * 1e3)
+            single.sort()
+            method["single_launch_bound_us"] = {"mean": statistics.mean(single), "p50": single[len(single) // 2],
+                                                "p99": single[int(len(single) * 0.99)], "samples": len(single),
+                                                "api": "Router.bind(...)() (metro_route_plan_launch_v1)"}
+            plan.close()
         else:
             # every step: 256 MiB L2 flush, NCCL all-gather of the local top-k ids,
             # routing kernel on the gathered batch; the flush-only loop is

@@ -186,6 +186,25 @@ METRO_API int metro_route_host_v1(const int32_t *topk_ids_host, int64_t num_pair
                                   void *dev_workspace, int32_t *host_out, int32_t *pair_rank_host,
                                   int32_t cluster_ctas, int32_t flags, void *stream);
 
+/* Launch plans for eager callers (no CUDA graph): the argument checks, the
+ * cluster / shared-memory plan and the kernel choice of metro_route_v1 /
+ * eplb_route_v1 done ONCE for fixed buffers, so each layer's launch is one call
+ * with two arguments.  kind: METRO_PLAN_METRO (metro_route_v1's arguments; x
+ * unused) or METRO_PLAN_EPLB (eplb_route_v1's; choice unused).  The buffers must
+ * stay allocated while the plan is used; num_pairs is fixed (a new batch size
+ * needs a new plan).  Same outputs, status words and parity as the one-shot
+ * entry points (routing.py:105-113 / :55-72). */
+#define METRO_PLAN_METRO 0
+#define METRO_PLAN_EPLB 1
+typedef struct metro_route_plan metro_route_plan;
+METRO_API int metro_route_plan_create_v1(int32_t kind, const int32_t *topk_ids, int64_t num_pairs,
+                                         const uint32_t *rank_mask, int32_t num_experts, int32_t num_ranks,
+                                         int32_t *loads, int32_t *choice, int32_t *x, int32_t *rank_counts,
+                                         int32_t *lam, int32_t *pair_rank, int32_t *status, int32_t cluster_ctas,
+                                         metro_route_plan **plan_out);
+METRO_API int metro_route_plan_launch_v1(const metro_route_plan *plan, void *stream);
+METRO_API int metro_route_plan_destroy_v1(metro_route_plan *plan);
+
 /* Programmatic dependent launch of the routing kernels (default on; METRO_PDL=0
  * in the environment or metro_set_pdl(0) turns it off).  With it a routing
  * kernel launched behind another kernel in the stream (the gating kernel in a

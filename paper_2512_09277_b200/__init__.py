@@ -43,7 +43,7 @@ from .routing import (
     run_router,
     save_assignment,
 )
-from .device import DevicePlacement, HostRouter, RouteResult, Router, ServedRouter, pack_placement
+from .device import DevicePlacement, HostRouter, RoutePlan, RouteResult, Router, ServedRouter, pack_placement
 from .dispatch import DispatchLayout, LayoutResult, replica_table
 from .io import (
     Trace,
@@ -64,7 +64,7 @@ __all__ = [
     "gen_zipf_topk", "gen_zipf_trace", "lambda_of", "make_placement", "route_bruteforce",
     "route_eplb", "route_metro", "route_metro_parallel", "route_optimal", "run_router",
     "save_assignment", "validate_assignment", "zipf_popularity",
-    "DevicePlacement", "HostRouter", "RouteResult", "Router", "ServedRouter", "pack_placement",
+    "DevicePlacement", "HostRouter", "RoutePlan", "RouteResult", "Router", "ServedRouter", "pack_placement",
     "NativeLibraryError", "Trace", "TraceBatch", "TraceFormatError", "load_placement", "load_trace",
     "load_trace_topk", "save_placement", "save_trace", "DispatchLayout", "LayoutResult", "replica_table",
 ]

@@ -32,6 +32,8 @@ ECUDA = -3
 ENOTBINARY = -4
 HOST_ZEROCOPY = 1
 HOST_STABLE_BUFFERS = 2
+PLAN_METRO = 0
+PLAN_EPLB = 1
 
 MAX_G = 128
 MAX_N = 4096
@@ -77,6 +79,9 @@ def lib() -> ctypes.CDLL:
         "metro_route_ordered_v1": ([P, i32, P, i32, i32, P, P, P, P, P], ctypes.c_int),
         "eplb_route_v1": ([P, i64, P, i32, i32, P, P, P, P, P, P, i32, P], ctypes.c_int),
         "eplb_route_from_loads_v1": ([P, P, i32, i32, P, P, P, P, P], ctypes.c_int),
+        "metro_route_plan_create_v1": ([i32, P, i64, P, i32, i32, P, P, P, P, P, P, P, i32, P], ctypes.c_int),
+        "metro_route_plan_launch_v1": ([P, P], ctypes.c_int),
+        "metro_route_plan_destroy_v1": ([P], ctypes.c_int),
         "metro_host_workspace_bytes": ([i64, i32, i32], ctypes.c_size_t),
         "metro_route_host_v1": ([P, i64, P, i32, i32, P, P, P, i32, i32, P], ctypes.c_int),
         "metro_debug_set_stamps": ([P], None),

@@ -738,15 +738,37 @@ int metro_pack_placement(const int8_t *A, int32_t N, int32_t G, uint32_t *mask) 
 
 static int effective_w(int G) { return words_for(G); }
 
-int metro_route_v1(const int32_t *ids, int64_t num_pairs, const uint32_t *mask, int32_t N,
-                   int32_t G, int32_t *loads, int32_t *choice, int32_t *rank_counts, int32_t *lam,
-                   int32_t *pair_rank, int32_t *status, int32_t cluster_ctas, void *stream) {
+}  // extern "C"
+
+// A planned routing launch: everything metro_route_v1 / eplb_route_v1 decide on
+// the host (argument checks, cluster size, staging, histogram copies, kernel
+// instance), kept so an eager caller re-launches with one call.
+using PlanLaunchFn = int (*)(const Params &, int, int, cudaStream_t);
+template <int W, bool PRIV>
+static int launch_metro_ids(const Params &p, int R, int smem, cudaStream_t s) {
+    return launch(metro_ids_kernel<W, PRIV>, R, smem, s, p);
+}
+template <int W, bool PAIR>
+static int launch_eplb_ids(const Params &p, int R, int smem, cudaStream_t s) {
+    return launch(eplb_ids_kernel<W, PAIR>, R, smem, s, p);
+}
+
+struct metro_route_plan {
+    Params p;
+    int R, smem;
+    PlanLaunchFn fn;
+};
+
+static int plan_metro(const int32_t *ids, int64_t num_pairs, const uint32_t *mask, int32_t N, int32_t G,
+                      int32_t *loads, int32_t *choice, int32_t *rank_counts, int32_t *lam, int32_t *pair_rank,
+                      int32_t *status, int32_t cluster_ctas, metro_route_plan &pl) {
     if ((!ids && num_pairs > 0) || !mask || !choice || !rank_counts || !lam || !status || num_pairs < 0)
         return METRO_EARG;
     int rc = check_dims(N, G);
     if (rc) return rc;
     const int W = effective_w(G);
-    Params p = {};
+    Params &p = pl.p;
+    p = Params{};
     p.ids = ids; p.num_pairs = num_pairs; p.mask = mask; p.N = N; p.G = G;
     p.loads = loads; p.choice = choice; p.rank_counts = rank_counts; p.lam = lam;
     p.pair_rank = pair_rank; p.status = status; p.stamps = g_stamps;
@@ -759,13 +781,82 @@ int metro_route_v1(const int32_t *ids, int64_t num_pairs, const uint32_t *mask, 
         smem = plan_ids(kMetroIds, false, num_pairs, N, W, cluster_ctas, p, R);
     }
     if (smem < 0) return smem;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    pl.R = R;
+    pl.smem = smem;
     if (priv) {
-        METRO_DISPATCH_W(W, return launch(metro_ids_kernel<kW, true>, R, smem, s, p));
+        METRO_DISPATCH_W(W, pl.fn = launch_metro_ids<kW, true>);
     } else {
-        METRO_DISPATCH_W(W, return launch(metro_ids_kernel<kW, false>, R, smem, s, p));
+        METRO_DISPATCH_W(W, pl.fn = launch_metro_ids<kW, false>);
     }
-    return METRO_EDIMS;
+    return METRO_OK;
+}
+
+static int plan_eplb(const int32_t *ids, int64_t num_pairs, const uint32_t *mask, int32_t N, int32_t G,
+                     int32_t *loads, int32_t *x, int32_t *rank_counts, int32_t *lam, int32_t *pair_rank,
+                     int32_t *status, int32_t cluster_ctas, metro_route_plan &pl) {
+    if ((!ids && num_pairs > 0) || !mask || !rank_counts || !lam || !status || num_pairs < 0)
+        return METRO_EARG;
+    int rc = check_dims(N, G);
+    if (rc) return rc;
+    const int W = effective_w(G);
+    Params &p = pl.p;
+    p = Params{};
+    p.ids = ids; p.num_pairs = num_pairs; p.mask = mask; p.N = N; p.G = G; p.loads = loads;
+    p.x32 = x; p.rank_counts = rank_counts; p.lam = lam; p.pair_rank = pair_rank; p.status = status;
+    int R = 1;
+    const int smem = plan_ids(kEplbIds, pair_rank != nullptr, num_pairs, N, W, cluster_ctas, p, R);
+    if (smem < 0) return smem;
+    pl.R = R;
+    pl.smem = smem;
+    if (pair_rank) {
+        METRO_DISPATCH_W(W, pl.fn = launch_eplb_ids<kW, true>);
+    } else {
+        METRO_DISPATCH_W(W, pl.fn = launch_eplb_ids<kW, false>);
+    }
+    return METRO_OK;
+}
+
+extern "C" {
+
+int metro_route_v1(const int32_t *ids, int64_t num_pairs, const uint32_t *mask, int32_t N,
+                   int32_t G, int32_t *loads, int32_t *choice, int32_t *rank_counts, int32_t *lam,
+                   int32_t *pair_rank, int32_t *status, int32_t cluster_ctas, void *stream) {
+    metro_route_plan pl;
+    const int rc = plan_metro(ids, num_pairs, mask, N, G, loads, choice, rank_counts, lam, pair_rank, status,
+                              cluster_ctas, pl);
+    if (rc) return rc;
+    return pl.fn(pl.p, pl.R, pl.smem, static_cast<cudaStream_t>(stream));
+}
+
+int metro_route_plan_create_v1(int32_t kind, const int32_t *ids, int64_t num_pairs, const uint32_t *mask,
+                               int32_t N, int32_t G, int32_t *loads, int32_t *choice, int32_t *x,
+                               int32_t *rank_counts, int32_t *lam, int32_t *pair_rank, int32_t *status,
+                               int32_t cluster_ctas, metro_route_plan **plan_out) {
+    if (!plan_out) return METRO_EARG;
+    *plan_out = nullptr;
+    metro_route_plan pl;
+    int rc;
+    if (kind == METRO_PLAN_METRO)
+        rc = plan_metro(ids, num_pairs, mask, N, G, loads, choice, rank_counts, lam, pair_rank, status,
+                        cluster_ctas, pl);
+    else if (kind == METRO_PLAN_EPLB)
+        rc = plan_eplb(ids, num_pairs, mask, N, G, loads, x, rank_counts, lam, pair_rank, status, cluster_ctas,
+                       pl);
+    else
+        rc = METRO_EARG;
+    if (rc) return rc;
+    *plan_out = new metro_route_plan(pl);
+    return METRO_OK;
+}
+
+int metro_route_plan_launch_v1(const metro_route_plan *pl, void *stream) {
+    if (!pl) return METRO_EARG;
+    return pl->fn(pl->p, pl->R, pl->smem, static_cast<cudaStream_t>(stream));
+}
+
+int metro_route_plan_destroy_v1(metro_route_plan *pl) {
+    delete pl;
+    return METRO_OK;
 }
 
 // Gating mode: plan like plan_ids, but every CTA's slice is whole tokens.
@@ -906,24 +997,11 @@ int metro_route_ordered_v1(const int32_t *order, int32_t m, const uint32_t *mask
 int eplb_route_v1(const int32_t *ids, int64_t num_pairs, const uint32_t *mask, int32_t N,
                   int32_t G, int32_t *loads, int32_t *x, int32_t *rank_counts, int32_t *lam,
                   int32_t *pair_rank, int32_t *status, int32_t cluster_ctas, void *stream) {
-    if ((!ids && num_pairs > 0) || !mask || !rank_counts || !lam || !status || num_pairs < 0)
-        return METRO_EARG;
-    int rc = check_dims(N, G);
+    metro_route_plan pl;
+    const int rc = plan_eplb(ids, num_pairs, mask, N, G, loads, x, rank_counts, lam, pair_rank, status,
+                             cluster_ctas, pl);
     if (rc) return rc;
-    const int W = effective_w(G);
-    Params p = {};
-    p.ids = ids; p.num_pairs = num_pairs; p.mask = mask; p.N = N; p.G = G; p.loads = loads;
-    p.x32 = x; p.rank_counts = rank_counts; p.lam = lam; p.pair_rank = pair_rank; p.status = status;
-    int R = 1;
-    const int smem = plan_ids(kEplbIds, pair_rank != nullptr, num_pairs, N, W, cluster_ctas, p, R);
-    if (smem < 0) return smem;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (pair_rank) {
-        METRO_DISPATCH_W(W, return launch(eplb_ids_kernel<kW, true>, R, smem, s, p));
-    } else {
-        METRO_DISPATCH_W(W, return launch(eplb_ids_kernel<kW, false>, R, smem, s, p));
-    }
-    return METRO_EDIMS;
+    return pl.fn(pl.p, pl.R, pl.smem, static_cast<cudaStream_t>(stream));
 }
 
 int eplb_route_from_loads_v1(const int64_t *loads, const uint32_t *mask, int32_t N, int32_t G,

@@ -24,8 +24,10 @@ def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
 
 
 def _stream(device: torch.device, stream: Optional[torch.cuda.Stream] = None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream(device)
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    # the raw handle of the device's current stream without building a Stream object
+    return torch._C._cuda_getCurrentRawStream(device.index)
 
 
 def _require_cuda(t: torch.Tensor, name: str, dtype: torch.dtype) -> torch.Tensor:
@@ -144,6 +146,27 @@ class Router:
         self.placement = placement
         self.kind = kind
         self.cluster_ctas = int(cluster_ctas)
+        self._checked = None
+        self._checked_ref = None  # keeps the checked result alive so its id() stays unique
+
+    def bind(self, topk_ids: torch.Tensor, out: Optional[RouteResult] = None, pair_rank: bool = True,
+             with_x: bool = False, stream: Optional[torch.cuda.Stream] = None) -> "RoutePlan":
+        """A launch plan for fixed buffers (metro_route_plan_create_v1): validation,
+        cluster plan and kernel choice happen here once; ``plan()`` then launches
+        one layer with a single two-argument C call -- the eager serving loop
+        that refills ``topk_ids`` in place each step.  Same outputs as route()."""
+        ids = _require_cuda(topk_ids, "topk_ids", torch.int32)
+        if ids.data_ptr() != topk_ids.data_ptr():
+            raise ValidationError("bind() needs a contiguous topk_ids buffer (it is read in place each launch)")
+        if ids.device != self.placement.device:
+            raise ValidationError(f"topk_ids on {ids.device}, placement on {self.placement.device}")
+        top_k = ids.shape[-1] if ids.dim() >= 2 else 1
+        num_pairs = ids.numel()
+        if out is None:
+            out = self.alloc(num_pairs, pair_rank=pair_rank, with_x=with_x, top_k=top_k)
+        else:
+            self._check_out(out, num_pairs)
+        return RoutePlan(self, ids, out, _stream(self.placement.device, stream))
 
     def alloc(self, num_pairs: int, pair_rank: bool = True, with_x: bool = False, top_k: int = 1) -> RouteResult:
         dev = self.placement.device
@@ -184,12 +207,18 @@ class Router:
               with_x: bool = False, stream: Optional[torch.cuda.Stream] = None) -> RouteResult:
         """Launch one routing kernel on ``stream`` (default: current stream)."""
         ids = _require_cuda(topk_ids, "topk_ids", torch.int32)
+        if ids.device != self.placement.device:
+            raise ValidationError(f"topk_ids on {ids.device}, placement on {self.placement.device}")
         top_k = ids.shape[-1] if ids.dim() >= 2 else 1
         num_pairs = ids.numel()
         if out is None:
             out = self.alloc(num_pairs, pair_rank=pair_rank, with_x=with_x, top_k=top_k)
-        else:
+        elif self._checked != (id(out), num_pairs):
+            # a result set is checked once per batch size; RouteResult's tensors are
+            # fixed at construction (replacing one means a new RouteResult)
             self._check_out(out, num_pairs)
+            self._checked = (id(out), num_pairs)
+            self._checked_ref = out
         L = _native.lib()
         p = self.placement
         s = _stream(p.device, stream)
@@ -260,6 +289,47 @@ class Router:
             _ptr(out.pair_rank), out.status.data_ptr(), ws, cl, s)
         _native.check_rc(rc, "metro_route_scores_v1")
         return topk_ids, out
+
+
+class RoutePlan:
+    """One routing launch planned for fixed buffers (Router.bind).  Calling it
+    launches the kernel on the bound stream and returns ``out``; refill
+    ``topk_ids`` in place between calls.  Holds its buffers alive; ``close()``
+    frees the C plan (also on garbage collection)."""
+
+    def __init__(self, router: Router, ids: torch.Tensor, out: RouteResult, stream: int):
+        p = router.placement
+        L = _native.lib()
+        h = ctypes.c_void_p()
+        kind = _native.PLAN_METRO if router.kind == "metro" else _native.PLAN_EPLB
+        rc = L.metro_route_plan_create_v1(
+            kind, ids.data_ptr(), ids.numel(), p.mask.data_ptr(), p.num_experts, p.num_ranks, _ptr(out.loads),
+            _ptr(out.choice), _ptr(out.x), out.rank_counts.data_ptr(), out.lam.data_ptr(), _ptr(out.pair_rank),
+            out.status.data_ptr(), router.cluster_ctas, ctypes.byref(h))
+        _native.check_rc(rc, "metro_route_plan_create_v1")
+        self.topk_ids, self.out, self.placement = ids, out, p
+        self._h = h
+        self._launch = L.metro_route_plan_launch_v1
+        self._args = (h, ctypes.c_void_p(stream))
+        self._destroy = L.metro_route_plan_destroy_v1
+
+    def __call__(self) -> RouteResult:
+        rc = self._launch(*self._args)
+        if rc:
+            _native.check_rc(rc, "metro_route_plan_launch_v1")
+        return self.out
+
+    def close(self) -> None:
+        if self._h is not None:
+            self._destroy(self._h)
+            self._h = None
+            self._args = (ctypes.c_void_p(0), self._args[1])  # a later call reports METRO_EARG
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def aggregate_loads_device(topk_ids: torch.Tensor, num_experts: int, cluster_ctas: int = 0,

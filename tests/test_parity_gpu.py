@@ -349,3 +349,54 @@ def test_pdl_chain_in_one_graph(shapes):
                 assert int(outs[j].lam.item()) == s["metro_lam"]
         finally:
             _native.lib().metro_set_pdl(1)
+
+
+def test_bound_plan_eager_loop(shapes):
+    """Router.bind (metro_route_plan_*): one plan per (buffers, batch size), the
+    ids refilled in place between launches, METRO and EPLB, every cluster size --
+    identical to route() and to the reference's golden outputs; route() with a
+    reused result set (checked once) stays exact too."""
+    from paper_2512_09277_b200 import _native
+
+    for name in ("ds", "q30", "q235_200"):
+        cs = [s for s in shapes if s["name"] == name]
+        if not cs:
+            continue
+        pl = DevicePlacement(cs[0]["A"])
+        for cl in (0, 1, 4):
+            ids = torch.empty(cs[0]["ids"].shape, dtype=torch.int32, device="cuda")
+            plan = Router(pl, "metro", cl).bind(ids)
+            eplan = Router(pl, "eplb", cl).bind(ids, with_x=True)
+            r = Router(pl, "metro", cl)
+            reuse = r.alloc(ids.numel(), top_k=ids.shape[1])
+            for s in cs:
+                ids.copy_(torch.from_numpy(s["ids"]))
+                o = plan().check()
+                e = eplan().check()
+                q = r.route(ids, out=reuse).check()
+                assert np.array_equal(o.choice.cpu().numpy(), s["metro_choice"]), (name, cl)
+                assert int(o.lam.item()) == s["metro_lam"]
+                assert np.array_equal(o.pair_rank.cpu().numpy(), oracle.pair_rank_metro(s["ids"].reshape(-1),
+                                                                                        s["metro_choice"]))
+                assert np.array_equal(q.choice.cpu().numpy(), s["metro_choice"])
+                assert np.array_equal(e.x.cpu().numpy(), s["eplb_x"])
+                assert int(e.lam.item()) == s["eplb_lam"]
+            plan.close()
+            with pytest.raises(pkg.ValidationError):
+                plan()
+    # a plan is capturable like route()
+    c = [s for s in shapes if s["name"] == "ds"][0]
+    pl = DevicePlacement(c["A"])
+    ids = torch.from_numpy(c["ids"]).cuda()
+    plan = Router(pl, "metro").bind(ids)
+    plan()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        plan_g = Router(pl, "metro").bind(ids, out=plan.out, stream=torch.cuda.current_stream())
+        plan_g()
+    plan.out.lam.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert int(plan.out.lam.item()) == c["metro_lam"]
+    assert _native.lib() is not None
