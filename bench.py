@@ -503,6 +503,21 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
                                                 "p99": single[int(len(single) * 0.99)], "samples": len(single),
                                                 "api": "Router.bind(...)() (metro_route_plan_launch_v1)"}
             plan.close()
+            # the floor of ANY eager launch measured this way on this box: a one-element
+            # torch kernel between the same two events
+            tiny = torch.zeros(1, device=dev)
+            single = []
+            for i in range(300):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record()
+                tiny.add_(1)
+                e1.record()
+                torch.cuda.synchronize()
+                single.append(e0.elapsed_time(e1) * 1e3)
+            method["single_launch_floor_us"] = {"p50": statistics.median(single),
+                                                "what": "torch one-element add between the same two events: "
+                                                        "the host launch path + launch latency of any kernel"}
         else:
             # every step: 256 MiB L2 flush, NCCL all-gather of the local top-k ids,
             # routing kernel on the gathered batch; the flush-only loop is

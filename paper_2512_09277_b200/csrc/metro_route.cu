@@ -567,6 +567,15 @@ static bool pdl_enabled() {
     return g_pdl != 0;
 }
 
+// METRO_R1_CLUSTER=1: launch one-CTA plans as a 1-CTA cluster (A/B of the launch path)
+static bool r1_plain() {
+    static const bool plain = [] {
+        const char *v = getenv("METRO_R1_CLUSTER");
+        return !(v && strcmp(v, "1") == 0);
+    }();
+    return plain;
+}
+
 template <typename K, typename... Args>
 static int launch(K kernel, int R, int smem, cudaStream_t s, Args... args) {
     cudaError_t e = prepare(kernel);
@@ -577,16 +586,23 @@ static int launch(K kernel, int R, int smem, cudaStream_t s, Args... args) {
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = R;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    int na = 0;
+    if (R > 1 || !r1_plain()) {  // one CTA: an ordinary launch (%cluster_nctarank reads 1)
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = R;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
     // programmatic dependent launch: every kernel launched here calls griddep_wait
     // before its first global access (METRO_PDL=0 disables, for A/B timing)
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    if (pdl_enabled()) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cfg.numAttrs = na;
     e = cudaLaunchKernelEx(&cfg, kernel, args...);
     if (e != cudaSuccess) return cuda_fail(e);
     return METRO_OK;
