@@ -57,6 +57,21 @@ METRO_API int metro_dispatch_layout_v1(const int32_t *topk_ids, const int32_t *p
                                        int32_t nrep, int32_t *pair_row, int32_t *rep_off, int32_t *status,
                                        int32_t cluster_ctas, void *stream);
 
+/* METRO routing fused with its dispatch layout in ONE launch: the outputs of
+ * metro_route_v1 (loads, choice, rank_counts, lam, pair_rank, status) and of
+ * metro_dispatch_layout_v1 on that routing (pair_row, rep_off), identical to the
+ * two launches chained.  A METRO expert has one active replica (e, choice[e])
+ * with T[e] rows (routing.py:46-50), so the layout needs only the histogram the
+ * routing already builds plus row-major occurrence ranks, which the kernel's
+ * idle warps compute while the serial greedy runs.  Falls back to the two
+ * launches when no fused plan fits shared memory (or for an empty batch).
+ * pair_rank and pair_row are required when num_pairs > 0. */
+METRO_API int metro_route_layout_v1(const int32_t *topk_ids, int64_t num_pairs, const uint32_t *rank_mask,
+                                    int32_t num_experts, int32_t num_ranks, const int32_t *rid_tab,
+                                    const int32_t *slot_base, int32_t nrep, int32_t *loads, int32_t *choice,
+                                    int32_t *rank_counts, int32_t *lam, int32_t *pair_rank, int32_t *pair_row,
+                                    int32_t *rep_off, int32_t *status, int32_t cluster_ctas, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -102,6 +102,7 @@ def lib() -> ctypes.CDLL:
         "metro_ipc_close_handle": ([P], ctypes.c_int),
         "metro_replica_table": ([P, i32, i32, P, P], ctypes.c_int),
         "metro_dispatch_layout_v1": ([P, P, i64, P, P, i32, i32, i32, P, P, P, i32, P], ctypes.c_int),
+        "metro_route_layout_v1": ([P, i64, P, i32, i32, P, P, i32, P, P, P, P, P, P, P, P, i32, P], ctypes.c_int),
     }
     for name, (argtypes, restype) in sig.items():
         fn = getattr(L, name)

@@ -54,7 +54,18 @@ struct Params {
     void *gate_ws;        // whole-GPU gating: int64 T[N] + routing-CTA counter, zero between launches
     int32_t gate_tokens;  // metro_gate_topk_kernel: tokens per CTA (<= kGateTokens)
     int32_t private_scratch;  // one-CTA plan: the sort scratch has its own shared memory (no alias of hist)
+    // fused dispatch layout (metro_route_layout_v1; include/dispatch_layout.h semantics)
+    const int32_t *rid_tab;    // [N, G] replica ids (-1: no replica), device
+    const int32_t *slot_base;  // [G + 1]
+    int32_t nrep;              // replicas; 0 = no fused layout
+    int32_t *pair_row;         // [num_pairs] row in the serving rank's receive buffer
+    int32_t *rep_off;          // [nrep + 1] exclusive row prefix per replica
+    int32_t dbg_skip;          // tuning only (METRO_DBG_SKIP): bit mask of fused-layout phases to skip
 };
+// walk warps of the fused layout: the warps NOT on warp 0's SM sub-partition (warp w
+// issues on SMSP w % 4; warp 0 runs the serial greedy meanwhile and keeps its SMSP)
+constexpr int kLayWarps = (kThreads / 32) * 3 / 4;
+__host__ __device__ constexpr int lay_index(int warp) { return (warp & 3) ? warp - 1 - (warp >> 2) : -1; }
 constexpr int kGateTokens = 2 * kThreads / 32;  // tokens per CTA in metro_gate_topk_kernel
 // auto policy of metro_route_scores_v1: above this many tokens the whole GPU takes
 // the top-k (measured crossover on B200: ~600 tokens at N = 256)
@@ -71,6 +82,9 @@ __device__ __forceinline__ void cta_sync() { asm volatile("bar.sync 1, %0;" ::"n
 // both are dead once the partial histograms have been reduced into T.
 struct Layout {
     int mbar, misc, mask, ids, T, choice, aux, hist, part, keys, cand, smask, sid, ent, rpart, sc, total;
+    // fused dispatch layout: replica table, slot bases, walk-warp occurrence counts /
+    // prefixes, per-pair in-warp ranks, CTA prefixes, rows / offsets per replica
+    int lrtab, lsb, lhw, locc, lpre, lrows, loff, lbase, lwsum;
     int NP;  // partial-row stride (words): N + 2 (bad pair lo/hi) rounded to 4
 };
 
@@ -81,10 +95,10 @@ constexpr int kES = 12;  // packed greedy entry stride (words)
 
 __host__ __device__ inline Layout make_layout(int kind, int N, int W, int R, int64_t slice,
                                               int C, int staged, bool warp_hist = false, int score_bytes = 0,
-                                              bool private_scratch = false) {
+                                              bool private_scratch = false, int lay_G = 0, int lay_nrep = 0) {
     Layout L;
     int o = 0;
-    L.mbar = o; o += 16;
+    L.mbar = o; o += 32;  // staging | partial exchange | fused-layout tables
     L.misc = o; o += 64 * 4;
     L.mask = o; o = align_up(o + N * W * 4, 16);
     L.NP = align_up(N + 2, 4);
@@ -113,6 +127,21 @@ __host__ __device__ inline Layout make_layout(int kind, int N, int W, int R, int
     L.rpart = align_up(L.ent + (W == 1 ? (N + 16) * kES * 4 : 0), 16);  // [4][N] partial ranks
     const int end2 = metro ? align_up(L.rpart + (4 * N + 16) * 4, 16) : o;  // + prefetch slack
     L.total = end1 > end2 ? end1 : end2;
+    // fused dispatch layout: regions of their own (live across the decide phase)
+    L.lrtab = L.lsb = L.lhw = L.locc = L.lpre = L.lrows = L.loff = L.lbase = L.lwsum = L.total;
+    if (lay_nrep > 0) {
+        int q = align_up(L.total, 16);
+        L.lrtab = q; q = align_up(q + N * lay_G * 4, 16);
+        L.lsb = q;   q = align_up(q + (lay_G + 1) * 4, 16);
+        L.lhw = q;   q = align_up(q + kLayWarps * N * 4, 16);
+        L.lrows = q; q = align_up(q + max(lay_nrep + 1, lay_G) * 4, 16);  // zeroed with lhw (contiguous)
+        L.locc = q;  q = align_up(q + static_cast<int>(slice) * 2, 16);
+        L.lpre = q;  q = align_up(q + N * 4, 16);
+        L.loff = q;  q = align_up(q + (lay_nrep + 1) * 4, 16);
+        L.lbase = q; q = align_up(q + N * 4, 16);
+        L.lwsum = q; q += 32 * 4;
+        L.total = q;
+    }
     // gating mode: the CTA's fp32 score rows, staged by TMA bulk copies
     L.sc = align_up(L.total, 128);
     if (score_bytes > 0) L.total = L.sc + score_bytes;
@@ -172,12 +201,25 @@ __device__ __forceinline__ StagePlan stage_plan(const Params &p, int64_t beg, in
     return s;
 }
 
+// fused layout: the replica table goes by one TMA bulk copy when it can
+__device__ __forceinline__ bool layout_rtab_bulk(const Params &p) {
+    return ((reinterpret_cast<uintptr_t>(p.rid_tab) & 15) == 0) && ((p.N * p.G) & 3) == 0;
+}
+
 // thread 0, first thing in the kernel: arm the mbarrier and launch the TMA copies
 __device__ __forceinline__ void stage_issue(const Params &p, const Layout &L, unsigned char *smem, int64_t beg,
                                             const StagePlan &s) {
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + L.mbar);
+    mbar_init(bar + 2, 1);  // fused layout: the replica table (read only after the decide phase)
     mbar_init(bar + 1, 1);  // partial-histogram exchange (st.async from the peer CTAs)
-    mbar_init(bar, 1);      // TMA staging (its init fence covers both)
+    mbar_init(bar, 1);      // TMA staging (its init fence covers all three)
+    if (p.nrep > 0 && layout_rtab_bulk(p)) {
+        const uint32_t rb = static_cast<uint32_t>(p.N * p.G * 4);
+        mbar_arrive_expect_tx(bar + 2, rb);
+        for (uint32_t o = 0; o < rb; o += 32768u)
+            bulk_g2s(smem + L.lrtab + o, reinterpret_cast<const unsigned char *>(p.rid_tab) + o, min(32768u, rb - o),
+                     bar + 2);
+    }
     uint32_t sc_bytes = 0;
     const float *sc_src = nullptr;
     if (p.score_bytes > 0) {  // gating mode: this CTA's rows of the score matrix
@@ -238,6 +280,7 @@ __device__ void histogram_push(const Params &p, const Layout &L, unsigned char *
     int32_t *s_part = reinterpret_cast<int32_t *>(smem + L.part);
     const int32_t *src = p.staged ? reinterpret_cast<const int32_t *>(smem + L.ids) : (p.ids + beg);
     int64_t my_bad = kNoBad;
+    int bad_i = INT32_MAX;  // first bad pair of this thread, relative to beg (32-bit min on the hot path)
 
     if (!COUNT) {
         // the gating stage already counted its ids into hist (gate_topk)
@@ -255,7 +298,7 @@ __device__ void histogram_push(const Params &p, const Layout &L, unsigned char *
                     if (static_cast<unsigned>(e) < static_cast<unsigned>(N))
                         atomicAdd(&s_hist[e * p.C + (lane & cm)], 1);
                     else
-                        my_bad = min(my_bad, beg + i + q);
+                        bad_i = min(bad_i, i + q);
                 }
             }
         }
@@ -264,8 +307,9 @@ __device__ void histogram_push(const Params &p, const Layout &L, unsigned char *
             if (static_cast<unsigned>(e) < static_cast<unsigned>(N))
                 atomicAdd(&s_hist[e * p.C + (lane & cm)], 1);
             else
-                my_bad = min(my_bad, beg + i);
+                bad_i = min(bad_i, i);
         }
+        if (bad_i != INT32_MAX) my_bad = beg + bad_i;
     } else {
         // warp-private histograms over contiguous warp sub-slices; match_any groups
         // equal ids so one lane does a plain read-modify-write.  The same walk later
@@ -331,10 +375,11 @@ __device__ void histogram_push(const Params &p, const Layout &L, unsigned char *
         for (int e = N + 2 + tid; e < L.NP; e += kThreads) row[e] = 0;
         cta_sync();
         const int nv = L.NP / 4;
-        for (int idx = tid; idx < static_cast<int>(R - 1) * nv; idx += kThreads) {
-            const uint32_t d = (rank + 1 + idx / nv) % R;
-            const int v = idx % nv;
-            st_async_v4(row + 4 * v, d, reinterpret_cast<const uint4 *>(row)[v], xbar);
+        for (uint32_t k = 1; k < R; ++k) {  // peers in rank order after this CTA (no division)
+            const uint32_t d = (rank + k < R) ? rank + k : rank + k - R;
+#pragma unroll 1
+            for (int v = tid; v < nv; v += kThreads)
+                st_async_v4(row + 4 * v, d, reinterpret_cast<const uint4 *>(row)[v], xbar);
         }
     } else if (!p.private_scratch) {
         // every thread's reads of the histogram counters are done before the decide
@@ -611,13 +656,81 @@ __device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t
     return L;
 }
 
+// Serial greedy in one warp for any G <= 128 (routing.py:94-101): lane owns ranks
+// g = lane + 32 k as packed keys (L << 8 | g): the warp-wide min over candidate
+// lanes is "smallest L, then smallest g" -- the reference's ascending scan with
+// strict '<'.  Per chunk of 32 steps the candidacy bits are transposed with
+// ballots (lane g gets bit s of step s), so the chain SEL -> redux.min -> ISETP ->
+// IADD touches no memory.  Warp 0 only; kept out of line (__noinline__).
+template <int W>
+__device__ __noinline__ void warp_greedy(const uint32_t *s_mask, int32_t *s_choice, const int32_t *s_sid,
+                                         const int32_t *s_L0, int G, int m2, int32_t *rank_counts, int32_t *lam,
+                                         bool writer) {
+    // (pointers and scalars only: a reference to the kernel's Params / Layout would
+    // put them on the stack)
+    const int lane = threadIdx.x & 31;
+        uint32_t Lk[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        const int g = lane + 32 * k;
+        Lk[k] = (g < G) ? ((static_cast<uint32_t>(s_L0[g]) << 8) | static_cast<uint32_t>(g)) : 0xffffffffu;
+    }
+    for (int base = 0; base < m2; base += 32) {
+        const int j = base + lane;
+        const bool v = j < m2;
+        const int myid = v ? s_sid[j] : 0;
+        uint32_t cb[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const uint32_t m = v ? s_mask[myid * W + k] : 0u;
+            cb[k] = 0;
+            const int gk = min(32, G - 32 * k);
+            for (int b = 0; b < gk; ++b) {
+                const unsigned bb = __ballot_sync(kFull, (m >> b) & 1u);
+                if (lane == b) cb[k] = bb;
+            }
+        }
+        const int steps = min(32, m2 - base);
+        uint32_t wmine = 0;
+#pragma unroll
+        for (int s = 0; s < 32; ++s) {
+            if (s >= steps) break;
+            uint32_t val = 0xffffffffu;
+#pragma unroll
+            for (int k = 0; k < W; ++k) val = ((cb[k] >> s) & 1u) ? min(val, Lk[k]) : val;
+            const uint32_t win = __reduce_min_sync(kFull, val);
+#pragma unroll
+            for (int k = 0; k < W; ++k) Lk[k] += (Lk[k] == win) ? 256u : 0u;
+            wmine = (lane == s) ? win : wmine;
+        }
+        if (v) s_choice[myid] = static_cast<int32_t>(wmine & 0xffu);
+    }
+    uint32_t mx = 0;
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        const int g = lane + 32 * k;
+        if (g < G) {
+            const uint32_t c = Lk[k] >> 8;
+            if (writer) rank_counts[g] = static_cast<int32_t>(c);
+            mx = max(mx, c);
+        }
+    }
+    mx = __reduce_max_sync(kFull, mx);
+    if (writer && lane == 0) *lam = static_cast<int32_t>(mx);
+}
+
 // Classify + sort + greedy.  MODE selects where T comes from: the cluster's
 // partial rows (kFromIds), the int64 loads argument (kFromLoads), or nowhere
 // (kFromOrder: a caller order, every listed expert goes through the greedy).
 // Returns false on error (status written by the writer CTA).
-template <int W, int MODE>
+struct NoOverlap {
+    __device__ __forceinline__ void operator()() const {}
+};
+// OV: work for warps 1.. while warp 0 runs the serial greedy (called once, by whole
+// warps, before the barrier that ends the greedy; e.g. the fused layout's walk)
+template <int W, int MODE, typename OV = NoOverlap>
 __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *smem, bool writer, uint32_t R,
-                             uint32_t rank) {
+                             uint32_t rank, const OV &overlap = OV()) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int N = p.N, G = p.G;
     int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
@@ -781,7 +894,7 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
     cta_sync();
     stamp(p, 5);
 
-    bool done = false;
+    bool done = false, overlap_done = false;
     if (MODE != kFromOrder && try_packed) {
         // Packed greedy (thread 0).  Valid iff every final counter is <= 126: the
         // counters only grow, so no byte ever crossed into the sign bit.
@@ -811,6 +924,8 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
             misc[M_PACKED_LO] = static_cast<int32_t>(Lp.lo);
             misc[M_PACKED_HI] = static_cast<int32_t>(Lp.hi);
         }
+        if (warp != 0) overlap();
+        overlap_done = true;
         cta_sync();
         done = misc[M_PACKED_OK] != 0;
         if (done) {  // the greedy thread stored every choice as it went
@@ -826,67 +941,127 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
         }
     }
     if (!done) {
-        // ---- serial greedy (routing.py:94-101) in warp 0, any G <= 128.
-        // Lane owns ranks g = lane + 32 k as packed keys (L << 8 | g): the warp-wide
-        // min over candidate lanes is "smallest L, then smallest g" -- the
-        // reference's ascending scan with strict '<'.  Per chunk of 32 steps the
-        // candidacy bits are transposed with ballots (lane g gets bit s of step s),
-        // so the chain SEL -> redux.min -> ISETP -> IADD touches no memory.
+        // ---- serial greedy (routing.py:94-101) in warp 0, any G <= 128 (out of
+        // line: its unrolled code stays out of the packed path's instruction stream)
         if (warp == 0) {
-            uint32_t Lk[W];
-#pragma unroll
-            for (int k = 0; k < W; ++k) {
-                const int g = lane + 32 * k;
-                Lk[k] = (g < G) ? ((static_cast<uint32_t>(s_L0[g]) << 8) | static_cast<uint32_t>(g)) : 0xffffffffu;
-            }
-            for (int base = 0; base < m2; base += 32) {
-                    const int j = base + lane;
-                const bool v = j < m2;
-                const int myid = v ? s_sid[j] : 0;
-                uint32_t cb[W];
-#pragma unroll
-                for (int k = 0; k < W; ++k) {
-                    const uint32_t m = v ? s_mask[myid * W + k] : 0u;
-                    cb[k] = 0;
-                    const int gk = min(32, G - 32 * k);
-                    for (int b = 0; b < gk; ++b) {
-                        const unsigned bb = __ballot_sync(kFull, (m >> b) & 1u);
-                        if (lane == b) cb[k] = bb;
-                    }
-                }
-                const int steps = min(32, m2 - base);
-                uint32_t wmine = 0;
-#pragma unroll
-                for (int s = 0; s < 32; ++s) {
-                    if (s >= steps) break;
-                    uint32_t val = 0xffffffffu;
-#pragma unroll
-                    for (int k = 0; k < W; ++k) val = ((cb[k] >> s) & 1u) ? min(val, Lk[k]) : val;
-                    const uint32_t win = __reduce_min_sync(kFull, val);
-#pragma unroll
-                    for (int k = 0; k < W; ++k) Lk[k] += (Lk[k] == win) ? 256u : 0u;
-                    wmine = (lane == s) ? win : wmine;
-                }
-                if (v) s_choice[myid] = static_cast<int32_t>(wmine & 0xffu);
-            }
-            uint32_t mx = 0;
-#pragma unroll
-            for (int k = 0; k < W; ++k) {
-                const int g = lane + 32 * k;
-                if (g < G) {
-                    const uint32_t c = Lk[k] >> 8;
-                    if (writer) p.rank_counts[g] = static_cast<int32_t>(c);
-                    mx = max(mx, c);
-                }
-            }
-            mx = __reduce_max_sync(kFull, mx);
-            if (writer && lane == 0) *p.lam = static_cast<int32_t>(mx);
+            warp_greedy<W>(s_mask, s_choice, s_sid, s_L0, G, m2, p.rank_counts, p.lam, writer);
+        } else if (!overlap_done) {
+            overlap();
         }
     }
     cta_sync();
     stamp(p, 6);
     return true;
 }
+
+// exclusive scan of v[0..n) into out[0..n], out[n] = total, over the kThreads
+// routing threads (three barriers)
+static __device__ __forceinline__ void block_exscan(const int32_t *v, int32_t *out, int n, int32_t *wsum) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (n + kThreads - 1) / kThreads;
+    const int b = min(n, tid * per), e = min(n, b + per);
+    int32_t s = 0;
+    for (int i = b; i < e; ++i) s += v[i];
+    int32_t x = s;  // inclusive warp scan
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int32_t y = __shfl_up_sync(kFull, x, d);
+        if (lane >= d) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    cta_sync();
+    if (warp == 0) {
+        int32_t w = lane < kWarps ? wsum[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int32_t y = __shfl_up_sync(kFull, w, d);
+            if (lane >= d) w += y;
+        }
+        if (lane < kWarps) wsum[lane] = w;  // inclusive warp totals
+    }
+    cta_sync();
+    int32_t run = x - s + (warp > 0 ? wsum[warp - 1] : 0);
+    for (int i = b; i < e; ++i) {
+        out[i] = run;
+        run += v[i];
+    }
+    if (tid == kThreads - 1) out[n] = wsum[kWarps - 1];
+    cta_sync();
+}
+
+// ---------------------------------------------------------------- fused dispatch layout
+// The dispatch layout of include/dispatch_layout.h computed inside the METRO
+// kernel.  A METRO expert has ONE active replica, (e, choice[e]), with T[e] rows
+// (routing.py:46-50, x[i, choice[i]] = T[i]), so
+//   pair_row[p] = rep_off[rid(e, g)] - rep_off[slot_base[g]]   (expert's first row on rank g)
+//               + occurrences of e in earlier CTAs' slices       (partial rows)
+//               + occurrences of e in earlier walk-warp sub-slices of this CTA
+//               + occurrences of e earlier in this warp's sub-slice (match_any)
+// with e = topk_ids[p], g = choice[e] -- pairs of one replica in row-major order,
+// the standalone layout kernel's convention.  The occurrence walk (walk-warp w =
+// warp - 1 owns a contiguous sub-slice) runs while warp 0 runs the greedy.
+struct LayoutWalk {
+    const Layout *L;
+    unsigned char *smem;
+    int n_local, N, ws;
+    int64_t *stamps;
+    int dbg;
+    __device__ __forceinline__ void operator()() const {
+        const int wi = lay_index(static_cast<int>(threadIdx.x >> 5));
+        if (wi < 0 || (dbg & 1)) return;
+        if (stamps && threadIdx.x == 32 && cluster_ctarank() == 0) stamps[30] = clock64();
+        walk(wi);
+        if (stamps && threadIdx.x == 32 && cluster_ctarank() == 0) stamps[26] = clock64();
+        // every walk warp's counts are in: exclusive prefixes over the walk warps,
+        // starting at the CTA prefix (occurrences in earlier CTAs' slices) -- still
+        // while warp 0 runs the greedy
+        asm volatile("bar.sync 2, %0;" ::"n"(kLayWarps * 32) : "memory");
+        uint32_t *s_hw = reinterpret_cast<uint32_t *>(smem + L->lhw);
+        const int32_t *s_pre = reinterpret_cast<const int32_t *>(smem + L->lpre);
+        for (int e = wi * 32 + static_cast<int>(threadIdx.x & 31); e < N; e += kLayWarps * 32) {
+            uint32_t run = static_cast<uint32_t>(s_pre[e]);
+            uint32_t c[kLayWarps];
+#pragma unroll
+            for (int w = 0; w < kLayWarps; ++w) c[w] = s_hw[w * N + e];
+#pragma unroll
+            for (int w = 0; w < kLayWarps; ++w) {
+                s_hw[w * N + e] = run;
+                run += c[w];
+            }
+        }
+        if (stamps && threadIdx.x == 32 && cluster_ctarank() == 0) stamps[29] = clock64();
+    }
+    __device__ __forceinline__ void walk(int w) const {
+        const int lane = threadIdx.x & 31;
+        const int32_t *s_ids = reinterpret_cast<const int32_t *>(smem + L->ids);
+        uint32_t *hw = reinterpret_cast<uint32_t *>(smem + L->lhw) + w * N;
+        uint16_t *occ = reinterpret_cast<uint16_t *>(smem + L->locc);
+        const int wb = min(n_local, w * ws), we = min(n_local, wb + ws);
+        // blocks of four chunks of 32 pairs: the id loads and match_any of the four
+        // chunks are independent (issued together); only the count updates chain
+        constexpr int U = 4;
+        for (int p0 = wb; p0 < we; p0 += 32 * U) {
+            int e[U];
+            unsigned m[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = p0 + 32 * u + lane;
+                e[u] = (i < we) ? s_ids[i] : -1;  // ids already range-checked
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) m[u] = __match_any_sync(kFull, e[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = p0 + 32 * u + lane;
+                if (e[u] >= 0) occ[i] = static_cast<uint16_t>(hw[e[u]] + __popc(m[u] & lanemask_lt()));
+                __syncwarp();
+                if (e[u] >= 0 && lane == __ffs(m[u]) - 1) hw[e[u]] += __popc(m[u]);
+                __syncwarp();
+            }
+        }
+    }
+};
+
 
 // ================================================================ kernels
 

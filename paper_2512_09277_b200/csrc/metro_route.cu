@@ -38,6 +38,7 @@
 #include <algorithm>
 #include <mutex>
 
+#include "../../include/dispatch_layout.h"
 #include "../../include/metro_route.h"
 #include "lib_internal.h"
 #include "metro_core.cuh"
@@ -45,12 +46,150 @@
 namespace metro {
 
 
-template <int W, bool PRIV, int GATE_NPL = 0>
+// Fused dispatch layout, after the decide phase (choice final; the walk warps
+// already turned their counts into exclusive prefixes during the greedy).  rep_off
+// is the exclusive scan over replica ids of the rows per replica, which for METRO
+// are T[e] on (e, choice[e]) and 0 elsewhere (routing.py:46-50); an expert's
+// first row on its rank is rep_off[rid(e, g)] - rep_off[slot_base[g]].  Every
+// step is one element per thread with a barrier between (serial per-warp chains
+// measured 2-3x slower on B200): scatter rows -> block scan (two barriers) ->
+// base + loads / choice -> pair_rank + pair_row of each walk warp's sub-slice.
+template <int W>
+__device__ void layout_tail(const Params &p, const Layout &L, unsigned char *smem, int64_t beg, int n_local,
+                            int ws, bool writer) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int N = p.N, G = p.G, nrep = p.nrep;
+    const int32_t *s_choice = reinterpret_cast<const int32_t *>(smem + L.choice);
+    const uint32_t *s_T = reinterpret_cast<const uint32_t *>(smem + L.T);
+    const int32_t *s_rtab = reinterpret_cast<const int32_t *>(smem + L.lrtab);
+    const int32_t *s_sb = reinterpret_cast<const int32_t *>(smem + L.lsb);
+    const uint32_t *s_hw = reinterpret_cast<const uint32_t *>(smem + L.lhw);
+    const uint16_t *s_occ = reinterpret_cast<const uint16_t *>(smem + L.locc);
+    int32_t *s_rows = reinterpret_cast<int32_t *>(smem + L.lrows);  // zeroed in the prologue
+    int32_t *s_off = reinterpret_cast<int32_t *>(smem + L.loff);
+    int32_t *s_base = reinterpret_cast<int32_t *>(smem + L.lbase);
+    int32_t *s_wsum = reinterpret_cast<int32_t *>(smem + L.lwsum);
+    if (layout_rtab_bulk(p)) mbar_wait(reinterpret_cast<uint64_t *>(smem + L.mbar) + 2, 0);
+    for (int e = tid; e < N; e += kThreads) {
+        const int g = s_choice[e];
+        if (g >= 0) s_rows[s_rtab[e * G + g]] = static_cast<int32_t>(s_T[e]);
+    }
+    cta_sync();
+    if (nrep <= kThreads) {
+        // one replica per thread: its inclusive warp scan and the warp totals go to
+        // shared memory, after ONE barrier any thread forms any offset (warp
+        // totals summed in registers) -- rep_off and the experts' first rows in the
+        // same pass
+        int32_t *s_incl = s_off;
+        const int32_t v = tid < nrep ? s_rows[tid] : 0;
+        int32_t x = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int32_t y = __shfl_up_sync(kFull, x, d);
+            if (lane >= d) x += y;
+        }
+        if (tid < nrep) s_incl[tid] = x;  // s_off holds nrep + 1 entries
+        if (lane == 31) s_wsum[warp] = x;
+        cta_sync();
+        int32_t ws_[kWarps];
+#pragma unroll
+        for (int q = 0; q < kWarps / 4; ++q) {
+            const int4 t4 = reinterpret_cast<const int4 *>(s_wsum)[q];
+            ws_[4 * q] = t4.x; ws_[4 * q + 1] = t4.y; ws_[4 * q + 2] = t4.z; ws_[4 * q + 3] = t4.w;
+        }
+        auto off = [&](int i) {  // exclusive prefix at replica i (i <= nrep)
+            const int wi = i >> 5;
+            int32_t o = (i & 31) ? s_incl[i - 1] : 0;
+#pragma unroll
+            for (int q = 0; q < kWarps; ++q) o += (q < wi) ? ws_[q] : 0;
+            return o;
+        };
+        if (writer && tid <= nrep) p.rep_off[tid] = off(tid);
+        for (int e = tid; e < N; e += kThreads) {
+            const int g = s_choice[e];
+            if (g >= 0) s_base[e] = off(s_rtab[e * G + g]) - off(s_sb[g]);
+            if (writer) {
+                if (p.loads) p.loads[e] = static_cast<int32_t>(s_T[e]);
+                p.choice[e] = g;
+            }
+        }
+    } else {
+        // block exclusive scan of rows[0..nrep): a contiguous chunk per thread, warp
+        // shuffle scan, warp totals through shared memory
+        const int per = (nrep + kThreads - 1) / kThreads;
+        const int b = min(nrep, tid * per), en = min(nrep, b + per);
+        int32_t sum = 0;
+        for (int i = b; i < en; ++i) sum += s_rows[i];
+        int32_t x = sum;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int32_t y = __shfl_up_sync(kFull, x, d);
+            if (lane >= d) x += y;
+        }
+        if (lane == 31) s_wsum[warp] = x;
+        cta_sync();
+        int32_t run = x - sum;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) run += (w < warp) ? s_wsum[w] : 0;
+        for (int i = b; i < en; ++i) {
+            const int32_t v = s_rows[i];
+            s_off[i] = run;
+            if (writer) p.rep_off[i] = run;
+            run += v;
+        }
+        if (tid == kThreads - 1) {
+            s_off[nrep] = run;  // the last thread's chunk ends the array
+            if (writer) p.rep_off[nrep] = run;
+        }
+        cta_sync();
+        for (int e = tid; e < N; e += kThreads) {
+            const int g = s_choice[e];
+            if (g >= 0) s_base[e] = s_off[s_rtab[e * G + g]] - s_off[s_sb[g]];
+            if (writer) {
+                if (p.loads) p.loads[e] = static_cast<int32_t>(s_T[e]);
+                p.choice[e] = g;
+            }
+        }
+    }
+    if (writer && tid == 0) {
+        p.status[0] = METRO_OK;
+        p.status[1] = p.status[2] = 0;
+        p.status[3] = static_cast<int32_t>(cluster_nctarank());
+    }
+    cta_sync();
+    const int w = lay_index(warp);
+    if (w < 0) return;
+    // walk warp w writes its own sub-slice: four pairs per lane (16-byte loads of
+    // the ids, 8-byte loads of the in-warp ranks, 16-byte stores), scalar tail
+    const int32_t *s_ids = reinterpret_cast<const int32_t *>(smem + L.ids);
+    const uint32_t *hw = s_hw + w * N;
+    const int wb = min(n_local, w * ws), we = min(n_local, wb + ws);
+    int32_t *pr = p.pair_rank + beg, *prow = p.pair_row + beg;
+    const bool vec = ((reinterpret_cast<uintptr_t>(pr) | reinterpret_cast<uintptr_t>(prow)) & 15) == 0;
+    const int we4 = vec ? wb + ((we - wb) & ~3) : wb;
+    for (int i = wb + 4 * lane; i < we4; i += 128) {
+        const int4 e = *reinterpret_cast<const int4 *>(s_ids + i);
+        const uint2 o = *reinterpret_cast<const uint2 *>(s_occ + i);
+        *reinterpret_cast<int4 *>(pr + i) = make_int4(s_choice[e.x], s_choice[e.y], s_choice[e.z], s_choice[e.w]);
+        *reinterpret_cast<int4 *>(prow + i) =
+            make_int4(s_base[e.x] + static_cast<int32_t>(hw[e.x]) + static_cast<int32_t>(o.x & 0xffffu),
+                      s_base[e.y] + static_cast<int32_t>(hw[e.y]) + static_cast<int32_t>(o.x >> 16),
+                      s_base[e.z] + static_cast<int32_t>(hw[e.z]) + static_cast<int32_t>(o.y & 0xffffu),
+                      s_base[e.w] + static_cast<int32_t>(hw[e.w]) + static_cast<int32_t>(o.y >> 16));
+    }
+    for (int i = we4 + lane; i < we; i += 32) {
+        const int e = s_ids[i];
+        pr[i] = s_choice[e];
+        prow[i] = s_base[e] + static_cast<int32_t>(hw[e]) + static_cast<int32_t>(s_occ[i]);
+    }
+}
+
+template <int W, bool PRIV, int GATE_NPL = 0, bool LAYOUT = false>
 __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t R = cluster_nctarank(), rank = cluster_ctarank();
     const Layout L = make_layout(kMetroIds, p.N, W, R, p.slice, p.C, p.staged, PRIV, p.score_bytes,
-                                 p.private_scratch != 0);
+                                 p.private_scratch != 0, LAYOUT ? p.G : 0, LAYOUT ? p.nrep : 0);
     const int64_t beg = static_cast<int64_t>(rank) * p.slice;
     const int64_t rem_pairs = p.num_pairs - beg;
     const int n_local = rem_pairs <= 0 ? 0 : static_cast<int>(rem_pairs < p.slice ? rem_pairs : p.slice);
@@ -61,11 +200,22 @@ __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) 
     int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
     init_misc(misc);
     zero_smem(smem, L.aux, L.part);  // forced counts + histogram
+    if (LAYOUT) zero_smem(smem, L.lhw, L.locc);  // walk-warp counts + rows per replica
     griddep_wait();
     griddep_launch_dependents();  // only once this kernel runs: at most one dependent waits
     if (threadIdx.x == 0) stage_issue(p, L, smem, beg, sp);
     if (R > 1) cluster_arrive_release();  // after thread 0 initialised the mbarriers
     stamp(p, 0);
+    // fused layout: the slot bases are loaded into a register now and stored to
+    // shared memory only after the decide phase's first barrier (the load's latency
+    // hides behind the histogram); the replica table goes by TMA when it can
+    int32_t sb_reg = 0;
+    if (LAYOUT) {
+        if (!layout_rtab_bulk(p))
+            for (int i = threadIdx.x; i < p.N * p.G; i += kThreads)
+                reinterpret_cast<int32_t *>(smem + L.lrtab)[i] = __ldg(p.rid_tab + i);
+        if (static_cast<int>(threadIdx.x) <= p.G) sb_reg = __ldg(p.slot_base + threadIdx.x);
+    }
     stage_rest(p, L, smem, beg, n_local, !GATE && p.staged != 0, sp);
     __syncthreads();
     if (GATE) {
@@ -98,6 +248,24 @@ __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) 
                 p.status[3] = static_cast<int32_t>(R);
             }
         }
+        return;
+    }
+    if (LAYOUT) {
+        // occurrences of each expert in earlier CTAs' slices, from the partial rows
+        // (read before the decide phase's scratch may reuse the exchange area)
+        int32_t *s_pre = reinterpret_cast<int32_t *>(smem + L.lpre);
+        const int32_t *s_part = reinterpret_cast<const int32_t *>(smem + L.part);
+        if (static_cast<int>(threadIdx.x) <= p.G) reinterpret_cast<int32_t *>(smem + L.lsb)[threadIdx.x] = sb_reg;
+        for (int e = threadIdx.x; e < p.N; e += kThreads) {
+            int32_t pre = 0;
+            for (uint32_t q = 0; q < rank; ++q) pre += s_part[q * L.NP + e];
+            s_pre[e] = pre;
+        }
+        const int ws = align_up((n_local + kLayWarps - 1) / kLayWarps, 32);
+        if (!metro_decide<W, kFromIds>(p, L, smem, writer, R, rank, LayoutWalk{&L, smem, n_local, p.N, ws, p.stamps, p.dbg_skip}))
+            return;
+        layout_tail<W>(p, L, smem, beg, n_local, ws, writer);
+        stamp(p, 7);
         return;
     }
     if (!metro_decide<W, kFromIds>(p, L, smem, writer, R, rank)) return;
@@ -665,7 +833,7 @@ static int check_dims(int N, int G) {
 // the layout fits 227 KB: prefer the requested / auto R, then a staged slice,
 // then more histogram copies.  Returns smem bytes or an error code.
 static int plan_ids(Kind kind, bool warp_hist, int64_t num_pairs, int N, int W, int requested,
-                    Params &p, int &R) {
+                    Params &p, int &R, int lay_G = 0, int lay_nrep = 0) {
     int cands[8], nc = 0;
     if (requested > 0) {
         if (requested != 1 && requested != 2 && requested != 4 && requested != 8 && requested != 16)
@@ -680,12 +848,15 @@ static int plan_ids(Kind kind, bool warp_hist, int64_t num_pairs, int N, int W, 
         slice = (slice + 3) & ~int64_t(3);
         if (slice < 4) slice = 4;
         if (slice > INT32_MAX / 8) continue;
-        for (int staged = 1; staged >= 0; --staged) {
+        // the fused layout walks the staged slice (uint16 in-warp ranks)
+        if (lay_nrep > 0 && slice > 65535) continue;
+        for (int staged = 1; staged >= (lay_nrep > 0 ? 1 : 0); --staged) {
             for (int C = copies_for(N); C >= 1; C >>= 1) {
                 // one CTA: prefer a sort scratch of its own (saves the barrier that
                 // orders the counter reads before the aliased scratch writes)
                 for (int priv = (r == 1 && kind == kMetroIds) ? 1 : 0; priv >= 0; --priv) {
-                    const Layout L = make_layout(kind, N, W, r, slice, C, staged, warp_hist, 0, priv != 0);
+                    const Layout L = make_layout(kind, N, W, r, slice, C, staged, warp_hist, 0, priv != 0, lay_G,
+                                                 lay_nrep);
                     if (L.total <= kMaxSmem) {
                         p.slice = slice;
                         p.staged = staged;
@@ -873,6 +1044,45 @@ int metro_route_plan_launch_v1(const metro_route_plan *pl, void *stream) {
 int metro_route_plan_destroy_v1(metro_route_plan *pl) {
     delete pl;
     return METRO_OK;
+}
+
+int metro_route_layout_v1(const int32_t *ids, int64_t num_pairs, const uint32_t *mask, int32_t N, int32_t G,
+                          const int32_t *rid_tab, const int32_t *slot_base, int32_t nrep, int32_t *loads,
+                          int32_t *choice, int32_t *rank_counts, int32_t *lam, int32_t *pair_rank,
+                          int32_t *pair_row, int32_t *rep_off, int32_t *status, int32_t cluster_ctas,
+                          void *stream) {
+    if ((!ids && num_pairs > 0) || !mask || !choice || !rank_counts || !lam || !status || num_pairs < 0 ||
+        !rid_tab || !slot_base || !rep_off || (num_pairs > 0 && (!pair_rank || !pair_row)))
+        return METRO_EARG;
+    int rc = check_dims(N, G);
+    if (rc) return rc;
+    if (nrep < 1 || nrep > 4096) return METRO_EDIMS;
+    const int W = effective_w(G);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Params p = {};
+    p.ids = ids; p.num_pairs = num_pairs; p.mask = mask; p.N = N; p.G = G;
+    p.loads = loads; p.choice = choice; p.rank_counts = rank_counts; p.lam = lam;
+    p.pair_rank = pair_rank; p.status = status; p.stamps = g_stamps;
+    p.rid_tab = rid_tab; p.slot_base = slot_base; p.nrep = nrep; p.pair_row = pair_row; p.rep_off = rep_off;
+    static const int dbg = [] {
+        const char *v = getenv("METRO_DBG_SKIP");
+        return v ? atoi(v) : 0;
+    }();
+    p.dbg_skip = dbg;
+    int R = 1;
+    const int smem = (hist_mode() == 1 && num_pairs > 0)
+                         ? plan_ids(kMetroIds, false, num_pairs, N, W, cluster_ctas, p, R, G, nrep)
+                         : METRO_EDIMS;
+    if (smem >= 0) {
+        METRO_DISPATCH_W(W, return launch(metro_ids_kernel<kW, false, 0, true>, R, smem, s, p));
+    }
+    // no fused plan fits (or an empty batch): routing, then the standalone layout
+    // kernel as its programmatic dependent -- the same outputs
+    rc = metro_route_v1(ids, num_pairs, mask, N, G, loads, choice, rank_counts, lam, pair_rank, status,
+                        cluster_ctas, stream);
+    if (rc) return rc;
+    return metro_dispatch_layout_v1(ids, pair_rank, num_pairs, rid_tab, slot_base, N, G, nrep, pair_row, rep_off,
+                                    status, 0, stream);
 }
 
 // Gating mode: plan like plan_ids, but every CTA's slice is whole tokens.

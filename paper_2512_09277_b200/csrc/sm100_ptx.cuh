@@ -36,12 +36,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 }
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));  // constant per CTA: CSE-able
     return r;
 }
 __device__ __forceinline__ uint32_t cluster_nctarank() {
     uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
     return r;
 }
 __device__ __forceinline__ void cluster_arrive_relaxed() {

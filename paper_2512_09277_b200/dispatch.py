@@ -21,7 +21,7 @@ import torch
 
 from . import _native
 from .core import ValidationError
-from .device import DevicePlacement, raise_status
+from .device import DevicePlacement, RouteResult, Router, raise_status
 
 
 def replica_table(A) -> Tuple[np.ndarray, np.ndarray]:
@@ -109,6 +109,51 @@ class DispatchLayout:
             ctypes.c_void_p(s.cuda_stream))
         _native.check_rc(rc, "metro_dispatch_layout_v1")
         return out
+
+    def alloc(self, num_pairs: int, top_k: int = 1) -> LayoutResult:
+        dev = self.placement.device
+        return LayoutResult(pair_row=torch.empty(max(num_pairs, 1), dtype=torch.int32, device=dev),
+                            rep_off=torch.empty(self.nrep + 1, dtype=torch.int32, device=dev),
+                            status=torch.empty(4, dtype=torch.int32, device=dev), top_k=top_k)
+
+    def route_metro(self, topk_ids: torch.Tensor, out: Optional[RouteResult] = None,
+                    layout_out: Optional[LayoutResult] = None, stream: Optional[torch.cuda.Stream] = None
+                    ) -> Tuple[RouteResult, LayoutResult]:
+        """METRO routing AND its dispatch layout in one launch
+        (metro_route_layout_v1): the same outputs as ``Router(placement,
+        "metro").route(ids)`` followed by ``self(ids, pair_rank)``.  The layout's
+        status words are the routing's (``layout_out.status`` is ``out.status``)."""
+        pl = self.placement
+        router = Router(pl, "metro", self.cluster_ctas)
+        ids = topk_ids.reshape(-1) if topk_ids.is_contiguous() else topk_ids.contiguous().reshape(-1)
+        if ids.dtype != torch.int32 or ids.device != pl.device:
+            raise ValidationError(f"topk_ids must be an int32 tensor on {pl.device}")
+        P = ids.numel()
+        top_k = topk_ids.shape[-1] if topk_ids.dim() == 2 else 1
+        if out is None:
+            out = router.alloc(max(P, 1), pair_rank=True, top_k=top_k)
+        else:
+            router._check_out(out, P)
+            if out.pair_rank is None:
+                raise ValidationError("out.pair_rank is required by the fused layout")
+        if layout_out is None:
+            layout_out = self.alloc(P, top_k)
+        else:
+            for name, t, n in (("pair_row", layout_out.pair_row, P), ("rep_off", layout_out.rep_off, self.nrep + 1)):
+                if (not isinstance(t, torch.Tensor) or t.dtype != torch.int32 or t.device != pl.device
+                        or not t.is_contiguous() or t.numel() < n):
+                    raise ValidationError(f"layout_out.{name} must be a contiguous int32 tensor of >= {n} "
+                                          f"elements on {pl.device}")
+        layout_out.status = out.status
+        s = stream if stream is not None else torch.cuda.current_stream(pl.device)
+        rc = _native.lib().metro_route_layout_v1(
+            ids.data_ptr() if P else None, P, pl.mask.data_ptr(), pl.num_experts, pl.num_ranks,
+            self.rid_tab.data_ptr(), self.slot_base.data_ptr(), self.nrep, out.loads.data_ptr(),
+            out.choice.data_ptr(), out.rank_counts.data_ptr(), out.lam.data_ptr(), out.pair_rank.data_ptr(),
+            layout_out.pair_row.data_ptr(), layout_out.rep_off.data_ptr(), out.status.data_ptr(),
+            self.cluster_ctas, ctypes.c_void_p(s.cuda_stream))
+        _native.check_rc(rc, "metro_route_layout_v1")
+        return out, layout_out
 
     def rank_groups(self, rep_off: np.ndarray, rank: int) -> List[Tuple[int, int, int]]:
         """(local slot, first row, rows) of every non-empty replica on ``rank``

@@ -196,3 +196,62 @@ def test_layout_errors(_cuda):
     badr[400] = 0  # pair 400 is expert 1, not hosted on rank 0
     with pytest.raises(ValidationError, match="token 400: rank 0 hosts no replica"):
         _dev_layout(ids, badr, A, 2)
+
+
+# ---------------------------------------------------------------- fused METRO + layout
+def _fused(ids, A, cluster=0):
+    pl = DevicePlacement(A)
+    dl = DispatchLayout(pl, cluster)
+    it = torch.as_tensor(np.ascontiguousarray(ids, np.int32)).cuda()
+    o, lo = dl.route_metro(it)
+    o.check()
+    P = int(np.size(ids))
+    return (o.loads.cpu().numpy(), o.choice.cpu().numpy(), o.rank_counts.cpu().numpy(), int(o.lam.item()),
+            o.pair_rank.cpu().numpy()[:P], lo.pair_row.cpu().numpy()[:P], lo.rep_off.cpu().numpy())
+
+
+def _check_fused(ids, A, cluster=0):
+    A = np.asarray(A, np.int8)
+    T = oracle.aggregate_loads(ids, A.shape[0])
+    choice, counts, lam = oracle.route_metro(T, A)
+    pr = oracle.pair_rank_metro(ids, choice).reshape(-1)
+    r0, o0 = oracle.dispatch_layout(ids, pr, A)
+    loads, ch, cnt, lm, pr1, r1, o1 = _fused(ids, A, cluster)
+    assert (loads == T).all() and (ch == choice).all() and (cnt == counts).all() and lm == lam
+    assert (pr1 == pr).all()
+    assert (o1 == o0).all()
+    assert (r1 == r0.reshape(-1)).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cluster", [0, 1, 2, 4, 8, 16])
+def test_fused_route_layout_golden(_cuda, shapes, cluster):
+    """metro_route_layout_v1 == metro_route_v1 + metro_dispatch_layout_v1 == the
+    oracle, on every golden shape at every cluster size (fallback included)."""
+    for c in shapes:
+        _check_fused(c["ids"], c["A"], cluster)
+
+
+@pytest.mark.gpu
+def test_fused_route_layout_fuzz_and_edges(_cuda):
+    rng = np.random.default_rng(11)
+    for it in range(150):
+        n = int(rng.integers(1, 400))
+        g = int(rng.choice([1, 2, 3, 8, 16, 33, 100]))
+        A = (rng.random((n, g)) < min(1.0, 3.0 / g)).astype(np.int8)
+        A[np.arange(n), rng.integers(0, g, n)] = 1
+        if A.sum() > 4096:
+            continue
+        B = int(rng.choice([0, 1, 5, 64, 255, 1024, 3000]))
+        k = int(rng.integers(1, min(10, n) + 1))
+        ids = rng.integers(0, n, (B, k)).astype(np.int32)  # duplicates allowed
+        _check_fused(ids, A, int(rng.choice([0, 1, 2, 4, 8, 16])))
+    # DeepSeek-V3 decode sweep through the auto plan
+    A = make_placement(256, 8, 1.5, 7).matrix
+    for B in (64, 256, 1024, 4096, 8192):
+        _check_fused(gen_zipf_topk(256, 8, B, 1.2, 77 + B, popularity_seed=7), A)
+    # an out-of-range id is reported like metro_route_v1
+    ids = gen_zipf_topk(256, 8, 64, 1.2, 5, popularity_seed=7)
+    ids[10, 3] = 999
+    with pytest.raises(ValidationError, match="token 10: expert id 999 out of range"):
+        _fused(ids, A)

@@ -4,6 +4,7 @@
     python tools/profile_target.py eplb [B]      # 8 EPLB launches, same inputs
     python tools/profile_target.py gate [B]      # 8 fused gating top-k + METRO launches (fp32 scores)
     python tools/profile_target.py dispatch [B]  # 8 dispatch-layout launches behind METRO routing
+    python tools/profile_target.py fused [B]     # 8 fused METRO + dispatch-layout launches
     python tools/profile_target.py exchange [B]  # 8 fused exchange + route launches, world 1
 """
 
@@ -44,6 +45,11 @@ def main():
         for b in batches:
             r.route(b, out=out)
             lay(b.reshape(-1), out.pair_rank)
+    elif what == "fused":
+        lay = DispatchLayout(pl)
+        out, lo = Router(pl, "metro").alloc(B * 8, top_k=8), lay.alloc(B * 8, 8)
+        for b in batches:
+            lay.route_metro(b, out=out, layout_out=lo)
     elif what == "exchange":
         routers, bufs = virtual_ranks(pl, 1, B, 8)
         for b in batches:
