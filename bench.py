@@ -461,6 +461,32 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
                 del graphs
             finally:
                 _native.lib().metro_set_pdl(1)
+            # routing + dispatch layout in ONE launch (metro_route_layout_v1) over the
+            # same pool, and the two-launch chain it replaces
+            from paper_2512_09277_b200 import DispatchLayout
+
+            dl = DispatchLayout(pl, args.cluster)
+            lo = dl.alloc(B * k, k)
+            n_l = min(max(K, 256), 2048)
+            fgraphs = []
+            for c0 in range(0, n_l, chunk):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    for j in range(c0, min(n_l, c0 + chunk)):
+                        dl.route_metro(big[j % P], out=out, layout_out=lo)
+                fgraphs.append(g)
+            method["route_layout_fused_us"] = timed(fgraphs, n_l)[0] * 1e3
+            del fgraphs
+            sgraphs = []
+            for c0 in range(0, n_l, chunk):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    for j in range(c0, min(n_l, c0 + chunk)):
+                        router.route(big[j % P], out=out)
+                        dl(big[j % P], out.pair_rank, out=lo)
+                sgraphs.append(g)
+            method["route_then_layout_us"] = timed(sgraphs, n_l)[0] * 1e3
+            del sgraphs
             del big
             # (b) context: eager launch after a 256 MiB L2 flush, flush time subtracted
             Kb = min(K, 2000)

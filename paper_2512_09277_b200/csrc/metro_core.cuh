@@ -64,8 +64,13 @@ struct Params {
 };
 // walk warps of the fused layout: the warps NOT on warp 0's SM sub-partition (warp w
 // issues on SMSP w % 4; warp 0 runs the serial greedy meanwhile and keeps its SMSP)
+#ifndef METRO_LAY_ALL_WARPS
 constexpr int kLayWarps = (kThreads / 32) * 3 / 4;
 __host__ __device__ constexpr int lay_index(int warp) { return (warp & 3) ? warp - 1 - (warp >> 2) : -1; }
+#else  // A/B: every warp but warp 0 walks
+constexpr int kLayWarps = kThreads / 32 - 1;
+__host__ __device__ constexpr int lay_index(int warp) { return warp - 1; }
+#endif
 constexpr int kGateTokens = 2 * kThreads / 32;  // tokens per CTA in metro_gate_topk_kernel
 // auto policy of metro_route_scores_v1: above this many tokens the whole GPU takes
 // the top-k (measured crossover on B200: ~600 tokens at N = 256)

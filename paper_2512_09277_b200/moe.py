@@ -301,6 +301,7 @@ class RankMoE:
 
         route (METRO / EPLB, pair ranks)      metro_route_v1 / eplb_route_v1
         -> dispatch layout                    metro_dispatch_layout_v1
+           (METRO: both in ONE launch,        metro_route_layout_v1)
         -> the rank's K3 work items           moe_layout_items_v1
         -> receive buffer (token rows)        moe_gather_rows_v1
         -> expert FFN                         moe_grouped_gemm_dev_v1, silu, GEMM
@@ -361,11 +362,16 @@ class RankMoE:
         s = stream if stream is not None else torch.cuda.current_stream(self.X.device)
         sp = ctypes.c_void_p(s.cuda_stream)
         L = _lib()
-        rr = self.router.route(topk_ids, out=self.route_out, stream=s)
         P = topk_ids.numel()
         ids = topk_ids.reshape(-1)
-        pr = rr.pair_rank[:P]
-        self.layout_out = self.layout(ids, pr, out=self.layout_out, stream=s)
+        if self.kind == "metro":  # routing + its dispatch layout in one launch
+            rr, self.layout_out = self.layout.route_metro(topk_ids, out=self.route_out,
+                                                          layout_out=self.layout_out, stream=s)
+            pr = rr.pair_rank[:P]
+        else:
+            rr = self.router.route(topk_ids, out=self.route_out, stream=s)
+            pr = rr.pair_rank[:P]
+            self.layout_out = self.layout(ids, pr, out=self.layout_out, stream=s)
         lo = self.layout_out
         _check(L.moe_layout_items_v1(lo.rep_off.data_ptr(), self.layout.slot_base.data_ptr(), self.rank,
                                      2 * self.ffn.inter, self.ffn.hidden, self.items1.data_ptr(), self.cap1,

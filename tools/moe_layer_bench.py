@@ -110,6 +110,15 @@ def run(batches=4, reps=5, B=1024, ratio=1.5, seed0=1000, dtype="bf16"):
             lout = pipe.layout_out
             res[kind]["dispatch_layout_us"] = time_graph(
                 lambda st: lay(ids, pr, out=lout, stream=st), reps, inner=200)
+            # routing + dispatch layout as the layer runs them (METRO: one fused launch)
+            rt, rout = pipe.router, pipe.route_out
+            if kind == "metro":
+                res[kind]["route_layout_us"] = time_graph(
+                    lambda st: lay.route_metro(ids, out=rout, layout_out=lout, stream=st), reps, inner=200)
+            else:
+                res[kind]["route_layout_us"] = time_graph(
+                    lambda st: (rt.route(ids, out=rout, stream=st), lay(ids, pr, out=lout, stream=st)), reps,
+                    inner=200)
             del pipe
         rows.append(res)
         print(json.dumps(res), file=sys.stderr, flush=True)
@@ -117,7 +126,7 @@ def run(batches=4, reps=5, B=1024, ratio=1.5, seed0=1000, dtype="bf16"):
     for kind in ("metro", "eplb"):
         summ[kind] = {key: statistics.mean(r[kind][key] for r in rows)
                       for key in ("activated", "tokens", "ffn_us", "weight_bytes", "achieved_gbs", "frac",
-                                  "device_layer_us", "dispatch_layout_us")}
+                                  "device_layer_us", "dispatch_layout_us", "route_layout_us")}
     summ["dtype"] = dtype
     summ["ffn_speedup_metro_vs_eplb"] = summ["eplb"]["ffn_us"] / summ["metro"]["ffn_us"]
     summ["device_layer_speedup_metro_vs_eplb"] = summ["eplb"]["device_layer_us"] / summ["metro"]["device_layer_us"]

@@ -7,7 +7,7 @@ tally (the evidence under profiles/<round>_soak.json).
 
 Entry points: METRO / EPLB routing from ids (every cluster size), METRO from
 loads and from an order (metro-parallel), fused gating (cluster + whole GPU),
-dispatch layout, the persistent host router, and the fused exchange with
+dispatch layout (standalone and fused with METRO routing), the persistent host router, and the fused exchange with
 virtual ranks.  Instances: N 1..700 experts, G 1..128 ranks (multi-word masks),
 k 1..10, batches 0..3000 tokens (Zipf or uniform ids, duplicates allowed),
 placements from the reference generator or random binary matrices.
@@ -134,8 +134,16 @@ def check_dispatch(ids, A, pl, t, o):
     lay = DispatchLayout(pl)
     res = lay(t, o.pair_rank.view(t.shape)).check()
     row, off = oracle.dispatch_layout(ids, o.pair_rank.cpu().numpy().reshape(ids.shape), A)
-    return {"dispatch": eq(res.pair_row.cpu().numpy().reshape(-1), np.asarray(row).reshape(-1))
-            and eq(res.rep_off.cpu().numpy()[:len(off)], off)}
+    ok = (eq(res.pair_row.cpu().numpy().reshape(-1), np.asarray(row).reshape(-1))
+          and eq(res.rep_off.cpu().numpy()[:len(off)], off))
+    # routing + layout fused in one launch (metro_route_layout_v1): must equal the chain
+    fo, fl = DispatchLayout(pl, int(np.random.default_rng(ids.size).choice(CLUSTERS))).route_metro(t)
+    fo.check()
+    okf = (eq(fo.choice.cpu(), o.choice.cpu()) and eq(fo.pair_rank.cpu(), o.pair_rank.cpu())
+           and int(fo.lam.item()) == int(o.lam.item())
+           and eq(fl.pair_row.cpu().numpy()[:ids.size], np.asarray(row).reshape(-1))
+           and eq(fl.rep_off.cpu().numpy()[:len(off)], off))
+    return {"dispatch": ok, "route_layout_fused": okf}
 
 
 def check_served(ids, A, pl):
