@@ -63,6 +63,24 @@ METRO_API int metro_allgather_route_v1(const int32_t *local_ids, int64_t local_p
                                        int32_t *local_pair_rank, int32_t *gathered_ids, int32_t *status,
                                        void *stream);
 
+/* The same exchange + METRO launch fused with the dispatch layout of the GLOBAL
+ * (rank-major) batch (include/dispatch_layout.h semantics): besides the routing
+ * outputs, local_pair_row [local_pairs] receives the row of each of this rank's
+ * pairs in its serving rank's receive buffer and rep_off [nrep + 1] the rows per
+ * replica (identical on every rank).  A pair's row needs only the exchanged
+ * per-rank histograms (occurrences of its expert in earlier ranks' slices) and
+ * the rank's own ids: no ids are gathered.  rid_tab / slot_base / nrep as
+ * metro_replica_table (dispatch_layout.h).  Limits: nrep <= 4096, local_pairs
+ * <= 65535.  Reference: the x[i, g] row counts of routing.py:41-52 charged by
+ * simulate.py:87-88. */
+METRO_API int metro_allgather_route_layout_v1(const int32_t *local_ids, int64_t local_pairs, int32_t rank,
+                                              int32_t world, void *const *peer_exchange, int64_t max_local_pairs,
+                                              const uint32_t *rank_mask, int32_t num_experts, int32_t num_ranks,
+                                              const int32_t *rid_tab, const int32_t *slot_base, int32_t nrep,
+                                              int32_t *loads, int32_t *choice, int32_t *rank_counts, int32_t *lam,
+                                              int32_t *local_pair_rank, int32_t *local_pair_row, int32_t *rep_off,
+                                              int32_t *status, void *stream);
+
 /* An exchange buffer of `bytes` (cudaMalloc'd as its own allocation, so a CUDA
  * IPC handle maps exactly it; zeroed, synchronous) and its release. */
 METRO_API int metro_exchange_alloc(size_t bytes, void **dev_ptr_out);

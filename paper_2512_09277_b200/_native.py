@@ -95,6 +95,8 @@ def lib() -> ctypes.CDLL:
         "metro_allgather_route_v1": ([P, i64, i32, i32, P, i64, P, i32, i32, P, P, P, P, P, P, P, P],
                                      ctypes.c_int),
         "metro_allgather_debug_stamps": ([P], None),
+        "metro_allgather_route_layout_v1": ([P, i64, i32, i32, P, i64, P, i32, i32, P, P, i32, P, P, P, P, P, P,
+                                             P, P, P], ctypes.c_int),
         "metro_exchange_alloc": ([ctypes.c_size_t, P], ctypes.c_int),
         "metro_exchange_free": ([P], ctypes.c_int),
         "metro_ipc_get_handle": ([P, P], ctypes.c_int),

@@ -81,12 +81,13 @@ __device__ __forceinline__ void xstamp(const XParams &x, int i) {
     if (x.stamps && threadIdx.x == 0) x.stamps[x.rank * 8 + i] = static_cast<int64_t>(x_now());
 }
 
-template <int W>
+template <int W, bool LAYOUT = false>
 __global__ void __launch_bounds__(kThreads, 1) metro_allgather_kernel(const XParams x) {
     extern __shared__ __align__(128) unsigned char smem[];
     const Params &p = x.p;
     const int tid = threadIdx.x, N = p.N, P = x.world, me = x.rank;
-    const Layout L = make_layout(kMetroIds, N, W, P, p.slice, p.C, 1);
+    const Layout L = make_layout(kMetroIds, N, W, P, p.slice, p.C, 1, false, 0, false, LAYOUT ? p.G : 0,
+                                 LAYOUT ? p.nrep : 0);
     const int n_local = static_cast<int>(p.num_pairs);
     const int XR = xrow_words(N);
     unsigned char *own = x.peers[me];
@@ -99,9 +100,19 @@ __global__ void __launch_bounds__(kThreads, 1) metro_allgather_kernel(const XPar
     int32_t *misc = reinterpret_cast<int32_t *>(smem + L.misc);
     init_misc(misc);
     zero_smem(smem, L.aux, L.part);
+    if (LAYOUT) zero_smem(smem, L.lhw, L.locc);  // walk-warp counts + rows per replica
     griddep_wait();
     griddep_launch_dependents();  // only once this kernel runs: at most one dependent waits
     if (tid == 0) stage_issue(p, L, smem, 0, sp);
+    // the dispatch layout's tables (as metro_ids_kernel<..., LAYOUT>): slot bases in a
+    // register until after the exchange, the replica table by TMA when it can
+    int32_t sb_reg = 0;
+    if (LAYOUT) {
+        if (!layout_rtab_bulk(p))
+            for (int i = tid; i < N * p.G; i += kThreads)
+                reinterpret_cast<int32_t *>(smem + L.lrtab)[i] = __ldg(p.rid_tab + i);
+        if (tid <= p.G) sb_reg = __ldg(p.slot_base + tid);
+    }
     stage_rest(p, L, smem, 0, n_local, true, sp);
     // (the threads that initialised these misc words: program order, no race)
     if (tid == X_EPOCH) misc[X_EPOCH] = static_cast<int32_t>(*reinterpret_cast<volatile uint32_t *>(own) + 1u);
@@ -278,6 +289,25 @@ __global__ void __launch_bounds__(kThreads, 1) metro_allgather_kernel(const XPar
     xstamp(x, 3);
 
     // ---- the METRO decision over T = sum of the P rows (identical on every rank)
+    if (LAYOUT) {
+        // this rank's pairs follow the earlier ranks' in the global (rank-major)
+        // order: their occurrences come first.  s_part row j holds rank (me + j) % P.
+        if (tid <= p.G) reinterpret_cast<int32_t *>(smem + L.lsb)[tid] = sb_reg;
+        int32_t *s_pre = reinterpret_cast<int32_t *>(smem + L.lpre);
+        for (int e = tid; e < N; e += kThreads) {
+            int32_t pre = 0;
+            for (int j = P - me; j < P; ++j) pre += s_part[j * L.NP + e];
+            s_pre[e] = pre;
+        }
+        const int ws = align_up((n_local + kLayWarps - 1) / kLayWarps, 32);
+        if (!metro_decide<W, kFromIds>(p, L, smem, true, static_cast<uint32_t>(P), 0,
+                                       LayoutWalk{&L, smem, n_local, N, ws, nullptr, 0}))
+            return;
+        xstamp(x, 4);
+        layout_tail<W>(p, L, smem, 0, n_local, ws, true, P);
+        xstamp(x, 5);
+        return;
+    }
     if (!metro_decide<W, kFromIds>(p, L, smem, true, static_cast<uint32_t>(P), 0)) return;
     xstamp(x, 4);
     const int32_t *s_choice = reinterpret_cast<const int32_t *>(smem + L.choice);
@@ -305,14 +335,14 @@ __global__ void __launch_bounds__(kThreads, 1) metro_allgather_kernel(const XPar
     xstamp(x, 5);
 }
 
-template <int W>
+template <int W, bool LAYOUT>
 static int x_launch(const XParams &x, int smem, cudaStream_t s) {
     static bool done[kMaxWorld] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < kMaxWorld && !done[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(metro_allgather_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kMaxSmem);
+        cudaError_t e = cudaFuncSetAttribute(metro_allgather_kernel<W, LAYOUT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
         if (e != cudaSuccess) return cuda_fail(e);
         done[dev] = true;
     }
@@ -326,7 +356,7 @@ static int x_launch(const XParams &x, int smem, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, metro_allgather_kernel<W>, x);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, metro_allgather_kernel<W, LAYOUT>, x);
     return e == cudaSuccess ? METRO_OK : cuda_fail(e);
 }
 
@@ -345,12 +375,20 @@ size_t metro_exchange_bytes(int32_t N, int32_t world, int64_t max_local_pairs) {
     return x_bytes(N, world, max_local_pairs);
 }
 
-int metro_allgather_route_v1(const int32_t *local_ids, int64_t local_pairs, int32_t rank, int32_t world,
-                             void *const *peer_exchange, int64_t max_local_pairs, const uint32_t *mask, int32_t N,
-                             int32_t G, int32_t *loads, int32_t *choice, int32_t *rank_counts, int32_t *lam,
-                             int32_t *local_pair_rank, int32_t *gathered_ids, int32_t *status, void *stream) {
+}  // extern "C"
+
+static int allgather_route(const int32_t *local_ids, int64_t local_pairs, int32_t rank, int32_t world,
+                           void *const *peer_exchange, int64_t max_local_pairs, const uint32_t *mask, int32_t N,
+                           int32_t G, int32_t *loads, int32_t *choice, int32_t *rank_counts, int32_t *lam,
+                           int32_t *local_pair_rank, int32_t *gathered_ids, int32_t *status, void *stream,
+                           const int32_t *rid_tab, const int32_t *slot_base, int32_t nrep, int32_t *pair_row,
+                           int32_t *rep_off) {
     if ((!local_ids && local_pairs > 0) || local_pairs < 0 || !peer_exchange || !mask || !choice || !rank_counts ||
         !lam || !status || world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
+        return METRO_EARG;
+    const bool layout = nrep > 0;
+    if (layout && (!rid_tab || !slot_base || !rep_off || nrep > 4096 ||
+                   (local_pairs > 0 && (!local_pair_rank || !pair_row))))
         return METRO_EARG;
     if (N < 1 || N > kMaxN || G < 1 || G > kMaxG) return METRO_EDIMS;
     if (gathered_ids && (local_pairs > max_local_pairs || (max_local_pairs & 3))) return METRO_EARG;
@@ -382,6 +420,9 @@ int metro_allgather_route_v1(const int32_t *local_ids, int64_t local_pairs, int3
     p.pair_rank = local_pair_rank;
     p.status = status;
     p.staged = 1;
+    if (layout) {
+        p.rid_tab = rid_tab; p.slot_base = slot_base; p.nrep = nrep; p.pair_row = pair_row; p.rep_off = rep_off;
+    }
     int64_t slice = (local_pairs + 3) & ~int64_t(3);
     if (slice < 4) slice = 4;
     p.slice = slice;
@@ -393,8 +434,9 @@ int metro_allgather_route_v1(const int32_t *local_ids, int64_t local_pairs, int3
     const int c0 = local_pairs > 2048 ? 32 : 8;
     for (int C = c0; C >= 1; C >>= 1) {
         if (C > 1 && N * C * 4 > 64 * 1024) continue;
-        const Layout L = make_layout(kMetroIds, N, W, world, slice, C, 1);
-        if (L.total <= kMaxSmem) {
+        const Layout L = make_layout(kMetroIds, N, W, world, slice, C, 1, false, 0, false, layout ? G : 0,
+                                     layout ? nrep : 0);
+        if (L.total <= kMaxSmem && (!layout || slice <= 65535)) {
             p.C = C;
             smem = L.total;
             break;
@@ -402,13 +444,45 @@ int metro_allgather_route_v1(const int32_t *local_ids, int64_t local_pairs, int3
     }
     if (smem < 0) return METRO_EDIMS;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (layout) {
+        switch (W) {
+            case 1: return x_launch<1, true>(x, smem, s);
+            case 2: return x_launch<2, true>(x, smem, s);
+            case 3: return x_launch<3, true>(x, smem, s);
+            case 4: return x_launch<4, true>(x, smem, s);
+            default: return METRO_EDIMS;
+        }
+    }
     switch (W) {
-        case 1: return x_launch<1>(x, smem, s);
-        case 2: return x_launch<2>(x, smem, s);
-        case 3: return x_launch<3>(x, smem, s);
-        case 4: return x_launch<4>(x, smem, s);
+        case 1: return x_launch<1, false>(x, smem, s);
+        case 2: return x_launch<2, false>(x, smem, s);
+        case 3: return x_launch<3, false>(x, smem, s);
+        case 4: return x_launch<4, false>(x, smem, s);
         default: return METRO_EDIMS;
     }
+}
+
+extern "C" {
+
+int metro_allgather_route_v1(const int32_t *local_ids, int64_t local_pairs, int32_t rank, int32_t world,
+                             void *const *peer_exchange, int64_t max_local_pairs, const uint32_t *mask, int32_t N,
+                             int32_t G, int32_t *loads, int32_t *choice, int32_t *rank_counts, int32_t *lam,
+                             int32_t *local_pair_rank, int32_t *gathered_ids, int32_t *status, void *stream) {
+    return allgather_route(local_ids, local_pairs, rank, world, peer_exchange, max_local_pairs, mask, N, G, loads,
+                           choice, rank_counts, lam, local_pair_rank, gathered_ids, status, stream, nullptr, nullptr,
+                           0, nullptr, nullptr);
+}
+
+int metro_allgather_route_layout_v1(const int32_t *local_ids, int64_t local_pairs, int32_t rank, int32_t world,
+                                    void *const *peer_exchange, int64_t max_local_pairs, const uint32_t *mask,
+                                    int32_t N, int32_t G, const int32_t *rid_tab, const int32_t *slot_base,
+                                    int32_t nrep, int32_t *loads, int32_t *choice, int32_t *rank_counts,
+                                    int32_t *lam, int32_t *local_pair_rank, int32_t *local_pair_row,
+                                    int32_t *rep_off, int32_t *status, void *stream) {
+    if (nrep < 1) return METRO_EDIMS;
+    return allgather_route(local_ids, local_pairs, rank, world, peer_exchange, max_local_pairs, mask, N, G, loads,
+                           choice, rank_counts, lam, local_pair_rank, nullptr, status, stream, rid_tab, slot_base,
+                           nrep, local_pair_row, rep_off);
 }
 
 int metro_exchange_alloc(size_t bytes, void **dev_ptr_out) {

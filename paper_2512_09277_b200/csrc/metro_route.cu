@@ -46,144 +46,6 @@
 namespace metro {
 
 
-// Fused dispatch layout, after the decide phase (choice final; the walk warps
-// already turned their counts into exclusive prefixes during the greedy).  rep_off
-// is the exclusive scan over replica ids of the rows per replica, which for METRO
-// are T[e] on (e, choice[e]) and 0 elsewhere (routing.py:46-50); an expert's
-// first row on its rank is rep_off[rid(e, g)] - rep_off[slot_base[g]].  Every
-// step is one element per thread with a barrier between (serial per-warp chains
-// measured 2-3x slower on B200): scatter rows -> block scan (two barriers) ->
-// base + loads / choice -> pair_rank + pair_row of each walk warp's sub-slice.
-template <int W>
-__device__ void layout_tail(const Params &p, const Layout &L, unsigned char *smem, int64_t beg, int n_local,
-                            int ws, bool writer) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int N = p.N, G = p.G, nrep = p.nrep;
-    const int32_t *s_choice = reinterpret_cast<const int32_t *>(smem + L.choice);
-    const uint32_t *s_T = reinterpret_cast<const uint32_t *>(smem + L.T);
-    const int32_t *s_rtab = reinterpret_cast<const int32_t *>(smem + L.lrtab);
-    const int32_t *s_sb = reinterpret_cast<const int32_t *>(smem + L.lsb);
-    const uint32_t *s_hw = reinterpret_cast<const uint32_t *>(smem + L.lhw);
-    const uint16_t *s_occ = reinterpret_cast<const uint16_t *>(smem + L.locc);
-    int32_t *s_rows = reinterpret_cast<int32_t *>(smem + L.lrows);  // zeroed in the prologue
-    int32_t *s_off = reinterpret_cast<int32_t *>(smem + L.loff);
-    int32_t *s_base = reinterpret_cast<int32_t *>(smem + L.lbase);
-    int32_t *s_wsum = reinterpret_cast<int32_t *>(smem + L.lwsum);
-    if (layout_rtab_bulk(p)) mbar_wait(reinterpret_cast<uint64_t *>(smem + L.mbar) + 2, 0);
-    for (int e = tid; e < N; e += kThreads) {
-        const int g = s_choice[e];
-        if (g >= 0) s_rows[s_rtab[e * G + g]] = static_cast<int32_t>(s_T[e]);
-    }
-    cta_sync();
-    if (nrep <= kThreads) {
-        // one replica per thread: its inclusive warp scan and the warp totals go to
-        // shared memory, after ONE barrier any thread forms any offset (warp
-        // totals summed in registers) -- rep_off and the experts' first rows in the
-        // same pass
-        int32_t *s_incl = s_off;
-        const int32_t v = tid < nrep ? s_rows[tid] : 0;
-        int32_t x = v;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int32_t y = __shfl_up_sync(kFull, x, d);
-            if (lane >= d) x += y;
-        }
-        if (tid < nrep) s_incl[tid] = x;  // s_off holds nrep + 1 entries
-        if (lane == 31) s_wsum[warp] = x;
-        cta_sync();
-        int32_t ws_[kWarps];
-#pragma unroll
-        for (int q = 0; q < kWarps / 4; ++q) {
-            const int4 t4 = reinterpret_cast<const int4 *>(s_wsum)[q];
-            ws_[4 * q] = t4.x; ws_[4 * q + 1] = t4.y; ws_[4 * q + 2] = t4.z; ws_[4 * q + 3] = t4.w;
-        }
-        auto off = [&](int i) {  // exclusive prefix at replica i (i <= nrep)
-            const int wi = i >> 5;
-            int32_t o = (i & 31) ? s_incl[i - 1] : 0;
-#pragma unroll
-            for (int q = 0; q < kWarps; ++q) o += (q < wi) ? ws_[q] : 0;
-            return o;
-        };
-        if (writer && tid <= nrep) p.rep_off[tid] = off(tid);
-        for (int e = tid; e < N; e += kThreads) {
-            const int g = s_choice[e];
-            if (g >= 0) s_base[e] = off(s_rtab[e * G + g]) - off(s_sb[g]);
-            if (writer) {
-                if (p.loads) p.loads[e] = static_cast<int32_t>(s_T[e]);
-                p.choice[e] = g;
-            }
-        }
-    } else {
-        // block exclusive scan of rows[0..nrep): a contiguous chunk per thread, warp
-        // shuffle scan, warp totals through shared memory
-        const int per = (nrep + kThreads - 1) / kThreads;
-        const int b = min(nrep, tid * per), en = min(nrep, b + per);
-        int32_t sum = 0;
-        for (int i = b; i < en; ++i) sum += s_rows[i];
-        int32_t x = sum;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int32_t y = __shfl_up_sync(kFull, x, d);
-            if (lane >= d) x += y;
-        }
-        if (lane == 31) s_wsum[warp] = x;
-        cta_sync();
-        int32_t run = x - sum;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) run += (w < warp) ? s_wsum[w] : 0;
-        for (int i = b; i < en; ++i) {
-            const int32_t v = s_rows[i];
-            s_off[i] = run;
-            if (writer) p.rep_off[i] = run;
-            run += v;
-        }
-        if (tid == kThreads - 1) {
-            s_off[nrep] = run;  // the last thread's chunk ends the array
-            if (writer) p.rep_off[nrep] = run;
-        }
-        cta_sync();
-        for (int e = tid; e < N; e += kThreads) {
-            const int g = s_choice[e];
-            if (g >= 0) s_base[e] = s_off[s_rtab[e * G + g]] - s_off[s_sb[g]];
-            if (writer) {
-                if (p.loads) p.loads[e] = static_cast<int32_t>(s_T[e]);
-                p.choice[e] = g;
-            }
-        }
-    }
-    if (writer && tid == 0) {
-        p.status[0] = METRO_OK;
-        p.status[1] = p.status[2] = 0;
-        p.status[3] = static_cast<int32_t>(cluster_nctarank());
-    }
-    cta_sync();
-    const int w = lay_index(warp);
-    if (w < 0) return;
-    // walk warp w writes its own sub-slice: four pairs per lane (16-byte loads of
-    // the ids, 8-byte loads of the in-warp ranks, 16-byte stores), scalar tail
-    const int32_t *s_ids = reinterpret_cast<const int32_t *>(smem + L.ids);
-    const uint32_t *hw = s_hw + w * N;
-    const int wb = min(n_local, w * ws), we = min(n_local, wb + ws);
-    int32_t *pr = p.pair_rank + beg, *prow = p.pair_row + beg;
-    const bool vec = ((reinterpret_cast<uintptr_t>(pr) | reinterpret_cast<uintptr_t>(prow)) & 15) == 0;
-    const int we4 = vec ? wb + ((we - wb) & ~3) : wb;
-    for (int i = wb + 4 * lane; i < we4; i += 128) {
-        const int4 e = *reinterpret_cast<const int4 *>(s_ids + i);
-        const uint2 o = *reinterpret_cast<const uint2 *>(s_occ + i);
-        *reinterpret_cast<int4 *>(pr + i) = make_int4(s_choice[e.x], s_choice[e.y], s_choice[e.z], s_choice[e.w]);
-        *reinterpret_cast<int4 *>(prow + i) =
-            make_int4(s_base[e.x] + static_cast<int32_t>(hw[e.x]) + static_cast<int32_t>(o.x & 0xffffu),
-                      s_base[e.y] + static_cast<int32_t>(hw[e.y]) + static_cast<int32_t>(o.x >> 16),
-                      s_base[e.z] + static_cast<int32_t>(hw[e.z]) + static_cast<int32_t>(o.y & 0xffffu),
-                      s_base[e.w] + static_cast<int32_t>(hw[e.w]) + static_cast<int32_t>(o.y >> 16));
-    }
-    for (int i = we4 + lane; i < we; i += 32) {
-        const int e = s_ids[i];
-        pr[i] = s_choice[e];
-        prow[i] = s_base[e] + static_cast<int32_t>(hw[e]) + static_cast<int32_t>(s_occ[i]);
-    }
-}
-
 template <int W, bool PRIV, int GATE_NPL = 0, bool LAYOUT = false>
 __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -264,7 +126,7 @@ __global__ void __launch_bounds__(kThreads, 1) metro_ids_kernel(const Params p) 
         const int ws = align_up((n_local + kLayWarps - 1) / kLayWarps, 32);
         if (!metro_decide<W, kFromIds>(p, L, smem, writer, R, rank, LayoutWalk{&L, smem, n_local, p.N, ws, p.stamps, p.dbg_skip}))
             return;
-        layout_tail<W>(p, L, smem, beg, n_local, ws, writer);
+        layout_tail<W>(p, L, smem, beg, n_local, ws, writer, static_cast<int32_t>(R));
         stamp(p, 7);
         return;
     }

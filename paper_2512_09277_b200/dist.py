@@ -139,7 +139,7 @@ class ExchangeRoute:
     """
 
     def __init__(self, placement: DevicePlacement, rank: int, world: int, local_tokens: int, top_k: int,
-                 peer_ptrs, max_local_pairs: int, gather_ids: bool = False):
+                 peer_ptrs, max_local_pairs: int, gather_ids: bool = False, layout=None):
         import ctypes
 
         from . import _native
@@ -161,6 +161,16 @@ class ExchangeRoute:
         self.gathered = torch.zeros((world * local_tokens, top_k), **i32) if gather_ids else None
         self._peers = (ctypes.c_void_p * world)(*[int(p) for p in peer_ptrs])
         self._fn = _native.lib().metro_allgather_route_v1
+        # optional dispatch layout of the global batch (metro_allgather_route_layout_v1):
+        # this rank's pairs' rows in their serving ranks' receive buffers + rep_off
+        self.layout = layout
+        self.layout_out = None
+        if layout is not None:
+            if gather_ids:
+                raise ValueError("the fused layout exchanges histograms only (gather_ids=False)")
+            self.layout_out = layout.alloc(self.local_pairs, top_k)
+            self.layout_out.status = self.out.status
+            self._fn_layout = _native.lib().metro_allgather_route_layout_v1
 
     def step(self, local_ids: Optional[torch.Tensor] = None,
              stream: Optional[torch.cuda.Stream] = None) -> RouteResult:
@@ -175,6 +185,16 @@ class ExchangeRoute:
         ids = ids.contiguous()
         s = (stream if stream is not None else torch.cuda.current_stream(p.device)).cuda_stream
         o = self.out
+        if self.layout is not None:
+            lo, lay = self.layout_out, self.layout
+            rc = self._fn_layout(ids.data_ptr(), self.local_pairs, self.rank, self.world, self._peers,
+                                 self.max_local_pairs, p.mask.data_ptr(), p.num_experts, p.num_ranks,
+                                 lay.rid_tab.data_ptr(), lay.slot_base.data_ptr(), lay.nrep, o.loads.data_ptr(),
+                                 o.choice.data_ptr(), o.rank_counts.data_ptr(), o.lam.data_ptr(),
+                                 o.pair_rank.data_ptr(), lo.pair_row.data_ptr(), lo.rep_off.data_ptr(),
+                                 o.status.data_ptr(), s)
+            _native.check_rc(rc, "metro_allgather_route_layout_v1")
+            return o
         rc = self._fn(ids.data_ptr(), self.local_pairs, self.rank, self.world, self._peers, self.max_local_pairs,
                       p.mask.data_ptr(), p.num_experts, p.num_ranks, o.loads.data_ptr(), o.choice.data_ptr(),
                       o.rank_counts.data_ptr(), o.lam.data_ptr(), o.pair_rank.data_ptr(),
@@ -213,7 +233,7 @@ def exchange_bytes(placement: DevicePlacement, world: int, max_local_pairs: int)
 
 
 def virtual_ranks(placement: DevicePlacement, world: int, local_tokens: int, top_k: int,
-                  gather_ids: bool = False):
+                  gather_ids: bool = False, layout=None):
     """``world`` EP ranks in ONE process on ONE device, each with its own exchange
     buffer, addressing the others' buffers directly: the same kernel and protocol
     as across GPUs (peer addresses are plain device addresses here).  Launch the
@@ -223,7 +243,7 @@ def virtual_ranks(placement: DevicePlacement, world: int, local_tokens: int, top
     nbytes = exchange_bytes(placement, world, max_local)
     bufs = [_ExchangeBuffer(nbytes, placement.device) for _ in range(world)]
     ptrs = [b.ptr.value for b in bufs]
-    routers = [ExchangeRoute(placement, r, world, local_tokens, top_k, ptrs, max_local, gather_ids)
+    routers = [ExchangeRoute(placement, r, world, local_tokens, top_k, ptrs, max_local, gather_ids, layout)
                for r in range(world)]
     return routers, bufs
 
@@ -238,7 +258,7 @@ class FusedAllGatherRouter(ExchangeRoute):
     """
 
     def __init__(self, placement: DevicePlacement, local_tokens: int, top_k: int, group=None,
-                 gather_ids: bool = False):
+                 gather_ids: bool = False, layout=None):
         import ctypes
 
         from . import _native
@@ -263,7 +283,7 @@ class FusedAllGatherRouter(ExchangeRoute):
                                                          ctypes.byref(p)), "metro_ipc_open_handle")
                 self._opened.append(p)
                 ptrs.append(p.value)
-        super().__init__(placement, rank, world, local_tokens, top_k, ptrs, max_local, gather_ids)
+        super().__init__(placement, rank, world, local_tokens, top_k, ptrs, max_local, gather_ids, layout)
         dist.barrier(group=group)
 
     def close(self):

@@ -155,3 +155,42 @@ def test_fused_allgather_empty_local_batches(world):
     finally:
         for b in bufs:
             b.close()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_fused_exchange_layout_matches_oracle(world, shapes):
+    """metro_allgather_route_layout_v1: every rank's own pairs' rows in the
+    GLOBAL (rank-major) dispatch layout and the replica offsets, from the
+    exchanged histograms only -- bit-exact with the oracle's layout of the
+    gathered batch under METRO (golden shapes + consecutive calls)."""
+    from paper_2512_09277_b200 import DispatchLayout
+
+    cases = [c for c in shapes if c["B"] % world == 0 and c["B"] * c["k"] // world <= 8192 and c["G"] <= 32]
+    for c in cases[:6]:
+        A = c["A"]
+        pl = DevicePlacement(A)
+        lay = DispatchLayout(pl)
+        B, k = c["B"], c["k"]
+        lt = B // world
+        routers, bufs = virtual_ranks(pl, world, lt, k, layout=lay)
+        streams = [torch.cuda.Stream() for _ in range(world)]
+        try:
+            for call in range(3):
+                ids = c["ids"] if call == 0 else gen_zipf_topk(c["N"], k, B, 1.2, 4000 + call, popularity_seed=7)
+                shards = [torch.from_numpy(np.ascontiguousarray(ids[r * lt:(r + 1) * lt])).cuda()
+                          for r in range(world)]
+                run_all(routers, shards, streams)
+                T = oracle.aggregate_loads(ids, A.shape[0])
+                choice, _, _ = oracle.route_metro(T, A)
+                pr = oracle.pair_rank_metro(ids, choice).reshape(-1)
+                row, off = oracle.dispatch_layout(ids, pr, A)
+                row = np.asarray(row).reshape(-1)
+                for rt in routers:
+                    check_rank(rt, ids, A, lt)
+                    lo = rt.layout_out
+                    own = slice(rt.rank * lt * k, (rt.rank + 1) * lt * k)
+                    assert np.array_equal(lo.pair_row.cpu().numpy()[:lt * k], row[own]), (c["name"], world, rt.rank)
+                    assert np.array_equal(lo.rep_off.cpu().numpy(), off), (c["name"], world)
+        finally:
+            for b in bufs:
+                b.close()
