@@ -57,6 +57,7 @@ for _s in (0.5, 2.0):
                                              skew=_s)
 
 POOL = 32          # distinct batches resident in HBM, cycled through the steps
+VIRTUAL = int(os.environ.get("METRO_VIRTUAL_RANKS", "0"))  # set in the --virtual-ranks children
 FLUSH_BYTES = 256 << 20
 POOL_BYTES = 256 << 20   # N=1 input pool (> 126 MB L2)
 SKEW = 1.2
@@ -75,6 +76,10 @@ def parse_args():
     ap.add_argument("--e2e-steps", type=int, default=1000)
     ap.add_argument("--detail", default=None, help="write extra per-run detail JSON here")
     ap.add_argument("--no-moe", action="store_true", help="skip the K3 expert-FFN measurement")
+    ap.add_argument("--virtual-ranks", type=int, default=0,
+                    help="run the N > 1 code path as P processes sharing ONE GPU (gloo plumbing, the fused "
+                         "exchange over CUDA IPC on one device): a dry run of the multi-GPU branch, not a "
+                         "scaling number")
     return ap.parse_args()
 
 
@@ -361,10 +366,13 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
             dist.barrier()
             torch.cuda.synchronize()
 
+    virtual = VIRTUAL > 1  # P ranks sharing one GPU over gloo (--virtual-ranks)
+    cdev = torch.device("cpu") if virtual else dev  # device of the plumbing collectives' tensors
+
     def max_over_ranks(vals):
         if world == 1:
             return vals
-        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        t = torch.tensor(vals, dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.tolist()
 
@@ -579,7 +587,7 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
                 bad = 0
             except Exception as ex:  # noqa: BLE001 -- reported in the JSON line
                 fused_err, bad = repr(ex)[:200], 1
-            flag = torch.tensor([bad], dtype=torch.int32, device=dev)
+            flag = torch.tensor([bad], dtype=torch.int32, device=cdev)
             dist.all_reduce(flag, op=dist.ReduceOp.MAX)
             if int(flag.item()) == 0:
                 tfz = loop_ms(K, lambda i: fz.step(local_pool[i % POOL]), True)
@@ -590,6 +598,18 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
                                     "NVLink peer stores); flush-only loop subtracted; one event pair per K-step "
                                     "loop; max over ranks")
                 method["nccl_allgather_plus_route_us"] = nccl_ms * 1e3
+                # the same exchange + route fused with the GLOBAL dispatch layout (rows of
+                # this rank's pairs in their serving ranks' receive buffers, no ids gather)
+                from paper_2512_09277_b200 import DispatchLayout
+
+                fzl = FusedAllGatherRouter(pl, lt, k, layout=DispatchLayout(pl))
+                for i in range(3):
+                    fzl.step(local_pool[i % POOL])
+                torch.cuda.synchronize()
+                tfl = loop_ms(K, lambda i: fzl.step(local_pool[i % POOL]), True)
+                method["fused_exchange_route_layout_us"] = max_over_ranks([(tfl - tf) / K])[0] * 1e3
+                sync_all()
+                fzl.close()
             else:
                 method["fused_unavailable"] = fused_err or "another rank failed"
             method["fused_exchange_route_us"] = None if fused_ms is None else fused_ms * 1e3
@@ -771,8 +791,45 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
     return res
 
 
+def run_virtual(args) -> int:
+    """--virtual-ranks P: launch P copies of this bench as ranks 0..P-1 of a gloo
+    process group, all on cuda:0 (torchrun's environment contract), and relay
+    rank 0's JSON line.  Exercises the N > 1 branch end to end on one GPU."""
+    import socket
+    import subprocess
+
+    P = args.virtual_ranks
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    argv = [a for a in sys.argv[1:]]
+    i = argv.index("--virtual-ranks") if "--virtual-ranks" in argv else -1
+    if i >= 0:
+        del argv[i:i + 2]
+    argv = [x for x in argv if not x.startswith("--virtual-ranks=")]
+    if "--gpus" in argv:
+        j = argv.index("--gpus")
+        del argv[j:j + 2]
+    procs = []
+    for r in range(P):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(P), LOCAL_RANK="0", LOCAL_WORLD_SIZE=str(P),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), METRO_VIRTUAL_RANKS=str(P))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), "--gpus", str(P)] + argv, env=env,
+                                      stdout=subprocess.PIPE if r == 0 else subprocess.DEVNULL, text=True))
+    out, _ = procs[0].communicate()
+    rcs = [procs[0].returncode] + [p.wait() for p in procs[1:]]
+    lines = [ln for ln in (out or "").splitlines() if ln.startswith("{")]
+    if any(rcs) or not lines:
+        print(json.dumps({"virtual_ranks": P, "error": f"rank exit codes {rcs}"}))
+        return 1
+    print(lines[-1])
+    return 0
+
+
 def main():
     args = parse_args()
+    if args.virtual_ranks > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(run_virtual(args))
     # a peer that never joins the fused exchange is reported after 2 s, never a hang
     os.environ.setdefault("METRO_PEER_TIMEOUT_MS", "2000")
     cfg = CONFIGS[args.config]
@@ -789,8 +846,15 @@ def main():
             import torch.distributed as dist
 
             torch.cuda.set_device(local_rank)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            if VIRTUAL > 1:  # ranks sharing one GPU: NCCL refuses that, gloo carries the plumbing
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         res = run_b200(args, cfg, rank, world, local_rank)
+        if res is not None and VIRTUAL > 1:
+            res["virtual_ranks"] = {"ranks": VIRTUAL, "note": "N > 1 code path on ONE GPU (P processes, gloo "
+                                    "plumbing, exchange over CUDA IPC on one device): a dry run, not a scaling "
+                                    "measurement"}
         if world > 1:
             import torch.distributed as dist
 

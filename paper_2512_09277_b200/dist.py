@@ -30,11 +30,15 @@ def allgather_topk(local_ids: torch.Tensor, out: Optional[torch.Tensor] = None, 
     if out is None:
         out = torch.empty((world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype,
                           device=local.device)
-    if local.is_cuda:
+    if local.is_cuda and dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, local, group=group)
-    else:  # gloo: list form
+    elif not local.is_cuda:  # gloo: list form
         parts = list(out.chunk(world, dim=0))
         dist.all_gather(parts, local, group=group)
+    else:  # CUDA tensors over gloo (ranks sharing a GPU): staged through host memory
+        parts = [torch.empty_like(local, device="cpu") for _ in range(world)]
+        dist.all_gather(parts, local.cpu(), group=group)
+        out.copy_(torch.cat(parts, dim=0))
     return out
 
 
