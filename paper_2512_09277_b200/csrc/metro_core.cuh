@@ -120,17 +120,25 @@ __host__ __device__ inline Layout make_layout(int kind, int N, int W, int R, int
     if (ids_mode) hist_bytes = warp_hist ? kWarps * N * 4 : N * C * 4;
     L.part = align_up(o + hist_bytes, 16);
     const int end1 = ids_mode ? align_up(L.part + R * L.NP * 4, 16) : L.part;
-    // the METRO sort scratch aliases hist + part (dead once T is reduced), unless the
-    // plan gives it its own space: then no barrier is needed between the last
-    // counter read and the first scratch write (one-CTA plans, histogram_push)
-    L.keys = (private_scratch && ids_mode && metro) ? end1 : o;
-    L.cand = align_up(L.keys + (N + 16) * 8, 16);
-    L.smask = L.cand;  // (unused: the warp greedy reads masks through sid)
-    L.sid = align_up(L.cand + N * 4, 16);
-    L.ent = align_up(L.sid + N * 4, 16);
-    // packed-greedy entries (W == 1 only), one slot per rank + readable padding
-    L.rpart = align_up(L.ent + (W == 1 ? (N + 16) * kES * 4 : 0), 16);  // [4][N] partial ranks
-    const int end2 = metro ? align_up(L.rpart + (4 * N + 16) * 4, 16) : o;  // + prefetch slack
+    // The METRO sort scratch aliases the histogram counters (dead once the partial
+    // rows are summed) when it fits inside them, unless the plan gives it its own
+    // space: then no barrier is needed between the last counter read and the
+    // first scratch write (one-CTA plans, histogram_push).  It never aliases the
+    // partial rows: classify reads them (every CTA's row of expert e, in passes
+    // of kThreads experts) while other threads already write sort keys.
+    auto scratch_at = [&](int keys) {
+        L.keys = keys;
+        L.cand = align_up(L.keys + (N + 16) * 8, 16);
+        L.smask = L.cand;  // (unused: the warp greedy reads masks through sid)
+        L.sid = align_up(L.cand + N * 4, 16);
+        L.ent = align_up(L.sid + N * 4, 16);
+        // packed-greedy entries (W == 1 only), one slot per rank + readable padding
+        L.rpart = align_up(L.ent + (W == 1 ? (N + 16) * kES * 4 : 0), 16);  // [4][N] partial ranks
+        return align_up(L.rpart + (4 * N + 16) * 4, 16);                    // + prefetch slack
+    };
+    int scratch_end = scratch_at(o);
+    if (ids_mode && metro && (private_scratch || scratch_end > L.part)) scratch_end = scratch_at(end1);
+    const int end2 = metro ? scratch_end : o;
     L.total = end1 > end2 ? end1 : end2;
     // fused dispatch layout: regions of their own (live across the decide phase)
     L.lrtab = L.lsb = L.lhw = L.locc = L.lpre = L.lrows = L.loff = L.lbase = L.lwsum = L.total;
@@ -1217,8 +1225,9 @@ __device__ void layout_tail(const Params &p, const Layout &L, unsigned char *sme
         if (g >= 0) s_rows[s_rtab[e * G + g]] = static_cast<int32_t>(s_T[e]);
     }
     cta_sync();
-    if (nrep <= kThreads) {
-        // one replica per thread: its inclusive warp scan and the warp totals go to
+    if (nrep < kThreads) {
+        // one replica per thread (and thread nrep writes the total, so nrep < kThreads):
+        // its inclusive warp scan and the warp totals go to
         // shared memory, after ONE barrier any thread forms any offset (warp
         // totals summed in registers) -- rep_off and the experts' first rows in the
         // same pass

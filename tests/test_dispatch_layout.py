@@ -7,6 +7,7 @@ bit-exact against the oracle for METRO and EPLB pair ranks at every cluster
 size, on fuzz, ragged/empty/maximum sizes and the error cases.
 """
 
+import os
 import numpy as np
 import pytest
 import torch
@@ -255,3 +256,55 @@ def test_fused_route_layout_fuzz_and_edges(_cuda):
     ids[10, 3] = 999
     with pytest.raises(ValidationError, match="token 10: expert id 999 out of range"):
         _fused(ids, A)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nrep", [31, 32, 33, 511, 512, 513, 1024])
+def test_fused_route_layout_replica_count_boundaries(_cuda, nrep):
+    """rep_off has nrep + 1 entries: replica counts at the one-replica-per-thread
+    limit of the fused scan (512 threads) and at warp multiples (found by the
+    soak: nrep == 512 lost rep_off[nrep])."""
+    rng = np.random.default_rng(nrep)
+    n, g = 256, 8
+    A = np.zeros((n, g), np.int8)
+    A[np.arange(n), np.arange(n) % g] = 1  # one replica each ...
+    extra = nrep - n
+    if extra < 0:
+        n = nrep
+        A = A[:n]
+    else:
+        free = np.argwhere(A == 0)
+        pick = free[rng.choice(len(free), extra, replace=False)]
+        A[pick[:, 0], pick[:, 1]] = 1  # ... plus extra replicas
+    assert int(A.sum()) == nrep
+    for B in (1, 255, 1024):
+        ids = rng.integers(0, n, (B, 8 if n >= 8 else n)).astype(np.int32)
+        for cluster in (0, 1, 4):
+            _check_fused(ids, A, cluster)
+
+
+@pytest.mark.gpu
+def test_fused_route_layout_large_tables(_cuda):
+    """Replica tables big enough that the plan shrinks the histogram copies: the
+    sort scratch must not alias the partial rows that classify still reads (two
+    soak instances, N > 512 experts x 65 ranks, that once routed wrong at R = 8),
+    plus a fuzz over N in (512, 700] and multi-word masks."""
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "fused_regress.npz"))
+    for i in (0, 1):
+        ids, A = z[f"ids{i}"], z[f"A{i}"]
+        for cluster in (0, 1, 2, 4, 8, 16):
+            _check_fused(ids, A, cluster)
+            T = oracle.aggregate_loads(ids, A.shape[0])
+            choice, counts, lam = oracle.route_metro(T, A)
+            o = Router(DevicePlacement(A), "metro", cluster).route(torch.from_numpy(ids).cuda()).check()
+            assert (o.choice.cpu().numpy() == choice).all() and int(o.lam.item()) == lam
+    rng = np.random.default_rng(5)
+    for _ in range(40):
+        n = int(rng.integers(513, 701))
+        g = int(rng.choice([33, 65, 100]))
+        A = (rng.random((n, g)) < rng.uniform(0.02, 0.1)).astype(np.int8)
+        A[np.arange(n), rng.integers(0, g, n)] = 1
+        if A.sum() > 4096:
+            continue
+        ids = rng.integers(0, n, (int(rng.choice([255, 1000, 3000])), int(rng.integers(1, 10)))).astype(np.int32)
+        _check_fused(ids, A, int(rng.choice([0, 2, 4, 8, 16])))
