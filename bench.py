@@ -57,6 +57,7 @@ for _s in (0.5, 2.0):
                                              skew=_s)
 
 POOL = 32          # distinct batches resident in HBM, cycled through the steps
+LAMBDA_SEEDS = 128  # fresh batches for the lambda statistics (>= 100 seeds)
 VIRTUAL = int(os.environ.get("METRO_VIRTUAL_RANKS", "0"))  # set in the --virtual-ranks children
 FLUSH_BYTES = 256 << 20
 POOL_BYTES = 256 << 20   # N=1 input pool (> 126 MB L2)
@@ -354,7 +355,6 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
     lt = B // world
     pl = DevicePlacement(A, dev)
     router = Router(pl, "metro", args.cluster)
-    eplb = Router(pl, "eplb", args.cluster)
     base = torch.from_numpy(np.stack(batches)).to(dev)  # [POOL, B, k] exact Zipf batches
     out = router.alloc(B * k, top_k=k)
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
@@ -615,14 +615,12 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
             method["fused_exchange_route_us"] = None if fused_ms is None else fused_ms * 1e3
         sync_all()
 
-    # lambda METRO vs EPLB over the exact Zipf batches (device outputs)
-    lam_m, lam_e = [], []
-    eout = eplb.alloc(B * k, pair_rank=False, top_k=k)
-    for b in base:
-        router.route(b, out=out).check()
-        eplb.route(b, out=eout, pair_rank=False).check()
-        lam_m.append(int(out.lam.item()))
-        lam_e.append(int(eout.lam.item()))
+    # lambda METRO vs EPLB through the device routers over >= 100 fresh Zipf batches
+    # (SURVEY.md §8(d)); Qwen3-235B: per physical GPU beside the per-column value
+    sys.path.insert(0, os.path.join(REPO, "tools"))
+    import lambda_stats
+
+    lam = lambda_stats.run(cfg, LAMBDA_SEEDS, dev, physical_group=2 if cfg["G"] == 16 else 0)
 
     # end to end from host buffers: H2D ids, route, D2H results, sync
     E = min(args.e2e_steps, K)
@@ -727,9 +725,9 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
                      "kernel": "metro_ids_kernel", "kernel_us": kern_ms * 1e3,
                      "note": "latency-bound serial greedy; HBM fraction is low by construction"},
         "timing": dict(method, allgather_us=ag_ms * 1e3, route_kernel_us=kern_ms * 1e3, timed_wall_s=wall),
-        "lambda": {"metro_mean": statistics.mean(lam_m), "eplb_mean": statistics.mean(lam_e),
-                   "metro_max": max(lam_m), "eplb_max": max(lam_e),
-                   "metro_le_eplb_all": all(a <= b for a, b in zip(lam_m, lam_e)), "batches": len(lam_m)},
+        "lambda": dict({"metro_mean": lam["metro"]["mean"], "eplb_mean": lam["eplb"]["mean"],
+                        "metro_max": lam["metro"]["max"], "eplb_max": lam["eplb"]["max"],
+                        "metro_le_eplb_all": lam["metro_le_eplb_all"], "batches": lam["seeds"]}, detail=lam),
         "clocks": clk.summary(),
     }
     if world > 1:

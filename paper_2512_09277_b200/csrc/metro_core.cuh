@@ -91,6 +91,7 @@ struct Layout {
     // prefixes, per-pair in-warp ranks, CTA prefixes, rows / offsets per replica
     int lrtab, lsb, lhw, locc, lpre, lrows, loff, lbase, lwsum;
     int NP;  // partial-row stride (words): N + 2 (bad pair lo/hi) rounded to 4
+    bool sync_part;  // the aliased sort scratch overlaps the partial rows (see make_layout)
 };
 
 __host__ __device__ inline int align_up(int x, int a) { return (x + a - 1) / a * a; }
@@ -120,12 +121,13 @@ __host__ __device__ inline Layout make_layout(int kind, int N, int W, int R, int
     if (ids_mode) hist_bytes = warp_hist ? kWarps * N * 4 : N * C * 4;
     L.part = align_up(o + hist_bytes, 16);
     const int end1 = ids_mode ? align_up(L.part + R * L.NP * 4, 16) : L.part;
-    // The METRO sort scratch aliases the histogram counters (dead once the partial
-    // rows are summed) when it fits inside them, unless the plan gives it its own
-    // space: then no barrier is needed between the last counter read and the
-    // first scratch write (one-CTA plans, histogram_push).  It never aliases the
-    // partial rows: classify reads them (every CTA's row of expert e, in passes
-    // of kThreads experts) while other threads already write sort keys.
+    // The METRO sort scratch aliases the histogram counters + partial rows (dead
+    // once T is reduced), unless the plan gives it its own space: then no barrier
+    // is needed between the last counter read and the first scratch write
+    // (one-CTA plans, histogram_push).  Classify reads the partial rows (every
+    // CTA's row of expert e, in passes of kThreads experts) while other threads
+    // already write sort keys, so when the keys can reach the partial rows
+    // (small C, large N) the rows are reduced into T behind a barrier first.
     auto scratch_at = [&](int keys) {
         L.keys = keys;
         L.cand = align_up(L.keys + (N + 16) * 8, 16);
@@ -136,8 +138,11 @@ __host__ __device__ inline Layout make_layout(int kind, int N, int W, int R, int
         L.rpart = align_up(L.ent + (W == 1 ? (N + 16) * kES * 4 : 0), 16);  // [4][N] partial ranks
         return align_up(L.rpart + (4 * N + 16) * 4, 16);                    // + prefetch slack
     };
-    int scratch_end = scratch_at(o);
-    if (ids_mode && metro && (private_scratch || scratch_end > L.part)) scratch_end = scratch_at(end1);
+    const bool priv = private_scratch && ids_mode && metro;
+    const int scratch_end = scratch_at(priv ? end1 : o);
+    // aliased scratch reaching into the partial rows: classify first sums every
+    // expert's rows into T, then a barrier, then the key writes (metro_decide)
+    L.sync_part = ids_mode && metro && !priv && scratch_end > L.part;
     const int end2 = metro ? scratch_end : o;
     L.total = end1 > end2 ? end1 : end2;
     // fused dispatch layout: regions of their own (live across the decide phase)
@@ -761,6 +766,14 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
     int m2 = 0;
     if (MODE != kFromOrder) {
         if (MODE == kFromIds) bad_min_warp0(L, smem, R, N);
+        if (MODE == kFromIds && L.sync_part) {  // T before any key write (make_layout)
+            for (int e = tid; e < N; e += kThreads) {
+                uint32_t t = 0;
+                for (uint32_t q = 0; q < R; ++q) t += static_cast<uint32_t>(s_part[q * L.NP + e]);
+                s_T[e] = t;
+            }
+            cta_sync();
+        }
         for (int base = 0; base < N; base += kThreads) {
             if (base + warp * 32 >= N) break;  // warp-uniform: no experts for this warp
             const int e = base + tid;
@@ -774,7 +787,9 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
                 r += __popc(mw[j]);
             }
             if (valid) {
-                if (MODE == kFromIds) {
+                if (MODE == kFromIds && L.sync_part) {
+                    t = s_T[e];
+                } else if (MODE == kFromIds) {
 #pragma unroll 4
                     for (uint32_t q = 0; q < R; ++q) t += static_cast<uint32_t>(s_part[q * L.NP + e]);
                 } else {

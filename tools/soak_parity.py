@@ -165,7 +165,11 @@ def check_exchange(rng, ids, A, pl):
     if B % world or B == 0 or A.shape[1] > 32 or A.shape[0] > 512:
         return {}
     lt = B // world
-    routers, bufs = virtual_ranks(pl, world, lt, k, gather_ids=True)
+    # every other call: the fused exchange + global dispatch layout variant
+    # (metro_allgather_route_layout_v1: histograms only, no ids gather)
+    with_layout = bool(rng.integers(2)) and int(A.sum()) <= 4096
+    lay = DispatchLayout(pl) if with_layout else None
+    routers, bufs = virtual_ranks(pl, world, lt, k, gather_ids=not with_layout, layout=lay)
     streams = [torch.cuda.Stream() for _ in range(world)]
     try:
         shards = [torch.from_numpy(np.ascontiguousarray(ids[r * lt:(r + 1) * lt])).cuda() for r in range(world)]
@@ -175,14 +179,21 @@ def check_exchange(rng, ids, A, pl):
         torch.cuda.synchronize()
         T = oracle.aggregate_loads(ids, A.shape[0])
         choice, counts, lam = oracle.route_metro(T, A)
+        if with_layout:
+            row, off = oracle.dispatch_layout(ids, oracle.pair_rank_metro(ids, choice), A)
+            row = np.asarray(row).reshape(-1)
         ok = True
         for rt in routers:
             rt.out.check()
             own = ids[rt.rank * lt:(rt.rank + 1) * lt]
             ok = ok and eq(rt.out.choice.cpu(), choice) and int(rt.out.lam.item()) == lam and \
-                eq(rt.out.pair_rank.cpu().numpy().reshape(own.shape), oracle.pair_rank_metro(own, choice)) and \
-                eq(rt.gathered.cpu(), ids)
-        return {"exchange": ok}
+                eq(rt.out.pair_rank.cpu().numpy().reshape(own.shape), oracle.pair_rank_metro(own, choice))
+            if with_layout:
+                ok = ok and eq(rt.layout_out.pair_row.cpu().numpy()[:lt * k], row[rt.rank * lt * k:(rt.rank + 1) * lt * k]) \
+                    and eq(rt.layout_out.rep_off.cpu().numpy()[:len(off)], off)
+            else:
+                ok = ok and eq(rt.gathered.cpu(), ids)
+        return {"exchange_layout" if with_layout else "exchange": ok}
     finally:
         for b in bufs:
             b.close()
