@@ -99,6 +99,11 @@ METRO_API int moe_silu_mul_dev_v1(const void *GU, int32_t T_cap, int32_t I, void
 
 /* cudaError_t of the last failing CUDA call of the MoE entry points (0 if none). */
 METRO_API int moe_last_cuda_error(void);
+/* Tuning only: per-CTA {start, end} globaltimer stamps (ns) of the next grouped-GEMM
+ * launches in this process, written to `stamps` (device, >= 2 x grid int64); NULL
+ * disables.  Not for production use. */
+METRO_API void moe_debug_set_stamps(int64_t *stamps);
+
 
 #ifdef __cplusplus
 }

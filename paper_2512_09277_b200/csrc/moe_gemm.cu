@@ -80,6 +80,7 @@ struct Params {
     int K;
     __nv_bfloat16 *Y;
     int ldy;
+    int64_t *stamps;  // tuning only (moe_debug_set_stamps): per CTA {start ns, end ns}
 };
 
 struct Maps {
@@ -229,6 +230,11 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (p.stamps && threadIdx.x == 0) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.stamps[2 * blockIdx.x] = static_cast<int64_t>(t);
+    }
 
     if (warp == 4) {
         // ---------------- TMA producer
@@ -331,6 +337,11 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (p.stamps && threadIdx.x == 0) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.stamps[2 * blockIdx.x + 1] = static_cast<int64_t>(t);
+    }
     if (warp == 5)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
                      : "memory");
@@ -534,6 +545,7 @@ __global__ void gather_rows_kernel(const uint4 *__restrict__ src, int row_vecs, 
 
 // ---------------------------------------------------------------- host
 static thread_local int g_err = 0;
+static int64_t *g_stamps = nullptr;  // moe_debug_set_stamps
 
 // launch with programmatic stream serialisation (every kernel above waits with
 // griddepcontrol.wait before touching its predecessors' outputs)
@@ -630,6 +642,7 @@ static int launch_gemm(const void *W, int32_t E, int32_t M, int32_t K, const voi
     prm.w_scale = w_scale;
     prm.x_scale = x_scale;
     prm.mblocks = M / BM;
+    prm.stamps = g_stamps;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool narrow = max_item_tokens <= NarrowTile::kN;
     cudaError_t e;
@@ -647,6 +660,8 @@ static int launch_gemm(const void *W, int32_t E, int32_t M, int32_t K, const voi
 }
 
 METRO_API int32_t moe_item_tokens(void) { return kItemTokens; }
+// tuning only: per-CTA {start, end} globaltimer stamps of the next grouped-GEMM launches
+METRO_API void moe_debug_set_stamps(int64_t *stamps) { g_stamps = stamps; }
 
 METRO_API int moe_grouped_gemm_v2(const void *W, int32_t E, int32_t M, int32_t K, const void *X, int32_t T,
                                   const int32_t *items, int32_t n_items, int32_t max_item_tokens, void *Y,
