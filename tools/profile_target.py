@@ -6,6 +6,8 @@
     python tools/profile_target.py dispatch [B]  # 8 dispatch-layout launches behind METRO routing
     python tools/profile_target.py fused [B]     # 8 fused METRO + dispatch-layout launches
     python tools/profile_target.py exchange [B]  # 8 fused exchange + route launches, world 1
+    python tools/profile_target.py regress [R]   # fused METRO + layout on the two large-table soak
+                                                 # instances (N > 512 x 65 ranks), cluster R (default 8)
 """
 
 import os
@@ -50,6 +52,18 @@ def main():
         out, lo = Router(pl, "metro").alloc(B * 8, top_k=8), lay.alloc(B * 8, 8)
         for b in batches:
             lay.route_metro(b, out=out, layout_out=lo)
+    elif what == "regress":
+        import numpy as np
+
+        z = np.load(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                                 "fused_regress.npz"))
+        cl = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+        for i in (0, 1):
+            ids, A2 = torch.from_numpy(z[f"ids{i}"]).to(dev), z[f"A{i}"]
+            pl2 = DevicePlacement(A2, dev)
+            lay = DispatchLayout(pl2, cl)
+            lay.route_metro(ids)[0].check()
+            Router(pl2, "metro", cl).route(ids).check()
     elif what == "exchange":
         routers, bufs = virtual_ranks(pl, 1, B, 8)
         for b in batches:

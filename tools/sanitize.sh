@@ -15,6 +15,11 @@ run "metro_ids_kernel" synccheck python tools/profile_target.py metro 256
 run "eplb_ids_kernel (profile_target.py eplb 256)" racecheck python tools/profile_target.py eplb 256
 run "layout_kernel (profile_target.py dispatch 256)" racecheck python tools/profile_target.py dispatch 256
 run "layout_kernel" memcheck python tools/profile_target.py dispatch 256
+run "fused METRO + layout (profile_target.py fused 1024)" racecheck python tools/profile_target.py fused 1024
+run "fused METRO + layout" memcheck python tools/profile_target.py fused 1024
+run "large tables N>512 x 65 ranks, R=8 (regress 8)" racecheck python tools/profile_target.py regress 8
+run "large tables N>512 x 65 ranks, R=1 (regress 1)" racecheck python tools/profile_target.py regress 1
+run "large tables N>512 x 65 ranks, R=8 (regress 8)" memcheck python tools/profile_target.py regress 8
 run "gating, cluster variant (gate 256)" racecheck python tools/profile_target.py gate 256
 run "gating, top-k grid + routing CTAs (gate 1024)" racecheck python tools/profile_target.py gate 1024
 run "gating, top-k grid + routing CTAs (gate 1024)" memcheck python tools/profile_target.py gate 1024
