@@ -257,6 +257,46 @@ def cpu_per_layer_stats(A, batches, reps: int = 400):
     return {"metro_layer_us": one(lambda b: oracle.metro_layer(b, A)), "eplb_layer_us": one(eplb_layer)}
 
 
+def python_reference_layer(cfg, A, batches, seconds: float = 1.0, min_reps: int = 200):
+    """Context only: the UNMODIFIED Python reference's layer --
+    eproute.aggregate_loads(TokenBatch) + eproute.routing.route_metro(T, A)
+    (core.py:236-244, routing.py:105-113) -- imported from baseline/_ref (the
+    offline install of /root/reference), on the same pinned core,
+    median over >= min_reps layers and >= `seconds`.  None when not installed."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "eproute")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        from eproute.core import ModelSpec, PlacementMap, Token, TokenBatch, aggregate_loads
+        from eproute.routing import route_metro
+    except Exception as ex:  # noqa: BLE001
+        return {"unavailable": f"{type(ex).__name__}: {ex}"}
+    G = cfg["G"]
+    model = ModelSpec(num_experts=cfg["N"], top_k=cfg["k"], hidden_dim=7168, dtype_bytes=2,
+                      expert_weight_bytes=1.0, dense_weight_bytes=1.0, flops_per_token_per_expert=1.0,
+                      num_moe_layers=1)
+    place = PlacementMap(matrix=np.asarray(A, np.int8), slots_per_gpu=int(np.asarray(A).sum(axis=0).max()))
+    tbs = [TokenBatch([Token(source_gpu=j % G, expert_ids=tuple(int(e) for e in row)) for j, row in enumerate(b)])
+           for b in batches[:8]]
+    per = []
+    with OneCore() as pin:
+        route_metro(aggregate_loads(tbs[0], model), place)
+        t_end = time.perf_counter() + seconds
+        i = 0
+        while time.perf_counter() < t_end or len(per) < min_reps:
+            t0 = time.perf_counter()
+            route_metro(aggregate_loads(tbs[i % len(tbs)], model), place)
+            per.append((time.perf_counter() - t0) * 1e6)
+            i += 1
+        core = pin.core
+    per.sort()
+    return {"what": "unmodified reference (baseline/_ref eproute 0.1.0): aggregate_loads + route_metro, CPython",
+            "median_us": per[len(per) // 2], "mean_us": statistics.mean(per), "p99_us": per[int(len(per) * 0.99)],
+            "reps": len(per), "cores": 1, "pinned_core": core}
+
+
 def cpu_allcores_throughput(A, batches, seconds: float = 2.0):
     """Independent layers on every host core (context only; one layer is serial)."""
     from concurrent.futures import ThreadPoolExecutor
@@ -316,7 +356,7 @@ def run_reference(args, cfg, rank: int, world: int):
         "arm": "reference algorithm's CPU path: the oracle port (oracle/metro_oracle.c), single thread, pinned",
         "cpu_baseline": {"value": us, "unit": "us/layer", "cores": 1, "kind": "port", "sample": sample,
                          "per_layer_us": st, "all_cores_layers_per_s": thr, "host_cores": cores,
-                         "cpu_model": cpu_model()},
+                         "cpu_model": cpu_model(), "python_reference": python_reference_layer(cfg, A, batches)},
         "e2e": {"value": us, "unit": "us/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -785,6 +825,7 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
                       "host core (the same function as --impl reference)",
             "per_layer_us": st, "all_cores_layers_per_s": thr, "host_cores": cores, "cpu_model": cpu_model(),
             "eplb_layer_us": cpu_per_layer_stats(A, batches)["eplb_layer_us"], "parity_vs_gpu": bool(parity),
+            "python_reference": python_reference_layer(cfg, A, batches),
         }
     return res
 
