@@ -661,6 +661,7 @@ def run_b200(args, cfg, rank: int, world: int, local_rank: int):
     import lambda_stats
 
     lam = lambda_stats.run(cfg, LAMBDA_SEEDS, dev, physical_group=2 if cfg["G"] == 16 else 0)
+    lam_m = lam.pop("metro_per_seed")  # seeds 1000 + s: the first POOL are this bench's exact batches
 
     # end to end from host buffers: H2D ids, route, D2H results, sync
     E = min(args.e2e_steps, K)

@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -631,7 +632,18 @@ static int launch_gemm(const void *W, int32_t E, int32_t M, int32_t K, const voi
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = num_ctas > 0 ? num_ctas : (n_items < sms ? n_items : sms);
+    // persistent CTAs, round-robin items.  Balanced grid: the fewest CTAs that keep
+    // the minimal number of waves (items per CTA), so every CTA gets the same item
+    // count (e.g. 2016 items: 144 CTAs x 14 instead of 148 with 92 x 14 + 56 x 13)
+    static const int balanced = [] {
+        const char *v = getenv("MOE_BALANCED_GRID");
+        return v ? atoi(v) : 0;
+    }();
+    int grid = num_ctas > 0 ? num_ctas : (n_items < sms ? n_items : sms);
+    if (num_ctas <= 0 && balanced && n_items > sms && !n_items_dev) {
+        const int waves = (n_items + sms - 1) / sms;
+        grid = (n_items + waves - 1) / waves;
+    }
     Params prm;
     prm.items = reinterpret_cast<const Item *>(items);
     prm.n_items = n_items;

@@ -61,3 +61,52 @@ def test_integration_section3_snippets():
     rows = int(layer.counts[2].item())
     assert rows == int((out.pair_rank.cpu().numpy() == g).sum())
     assert torch.isfinite(y[:rows].float()).all()
+
+    # METRO routing and its layout in one launch
+    out3, res3 = lay.route_metro(topk_ids)
+    out3.check()
+    assert torch.equal(out3.pair_rank.reshape(-1)[:B * k], out.pair_rank.reshape(-1)[:B * k])
+    assert torch.equal(res3.pair_row.reshape(-1)[:B * k], res.pair_row.reshape(-1)[:B * k])
+    assert torch.equal(res3.rep_off, res.rep_off)
+
+    # eager callers: a bound launch plan
+    buf = topk_ids.clone()
+    out4 = router.alloc(num_pairs=B * k, top_k=k)
+    launch = router.bind(buf, out4)
+    launch()
+    out4.check()
+    assert torch.equal(out4.choice, out.choice) and torch.equal(out4.pair_rank, out.pair_rank)
+
+
+def test_integration_fused_exchange_layout_snippet():
+    """§3's FusedAllGatherRouter(..., layout=lay) on one rank (world 1): its own
+    pairs' rows equal the layout of the whole batch."""
+    import torch.distributed as dist
+
+    from paper_2512_09277_b200.dispatch import DispatchLayout
+    from paper_2512_09277_b200.dist import FusedAllGatherRouter
+
+    device = torch.device("cuda", 0)
+    A = make_placement(256, 8, 1.5, 7).matrix
+    B, k = 256, 8
+    topk = gen_zipf_topk(256, k, B, 1.2, 78, popularity_seed=7)
+    topk_ids = torch.from_numpy(topk).to(device)
+    placement = DevicePlacement(A, device)
+    lay = DispatchLayout(placement)
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("gloo", init_method="tcp://127.0.0.1:29631", rank=0, world_size=1)
+    try:
+        fzl = FusedAllGatherRouter(placement, local_tokens=B, top_k=k, layout=lay)
+        out = fzl.step(topk_ids)
+        out.check()
+        T = oracle.aggregate_loads(topk, 256)
+        choice, counts, lam = oracle.route_metro(T, A)
+        row, off = oracle.dispatch_layout(topk, oracle.pair_rank_metro(topk, choice), A)
+        assert np.array_equal(out.choice.cpu().numpy(), choice)
+        assert np.array_equal(fzl.layout_out.pair_row.cpu().numpy()[:B * k], np.asarray(row).reshape(-1))
+        assert np.array_equal(fzl.layout_out.rep_off.cpu().numpy()[:len(off)], off)
+        fzl.close()
+    finally:
+        if own:
+            dist.destroy_process_group()

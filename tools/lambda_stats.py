@@ -53,7 +53,7 @@ def run(cfg: dict, seeds: int = 128, device=None, physical_group: int = 0) -> di
             ce = oe.rank_counts.cpu().numpy().reshape(-1, physical_group).sum(axis=1)
             pm.append(int(cm.max()))
             pe.append(int(ce.max()))
-    res = {"seeds": seeds, "metro": _summ(lm), "eplb": _summ(le),
+    res = {"seeds": seeds, "metro": _summ(lm), "eplb": _summ(le), "metro_per_seed": lm,
            "eplb_over_metro_mean": statistics.mean(e / m for e, m in zip(le, lm) if m > 0) if any(lm) else None,
            "metro_le_eplb_all": all(a <= b for a, b in zip(lm, le)),
            "metro_lt_eplb_batches": sum(a < b for a, b in zip(lm, le))}
@@ -77,6 +77,7 @@ def main():
     out = {}
     for name, cfg in bench.CONFIGS.items():
         r = run(cfg, a.seeds, physical_group=2 if cfg["G"] == 16 else 0)
+        r.pop("metro_per_seed")
         out[name] = dict(r, workload=cfg["workload"])
         line = f"{name}: METRO {r['metro']['mean']:.2f} vs EPLB {r['eplb']['mean']:.2f} ({a.seeds} seeds)"
         if "per_physical_gpu" in r:

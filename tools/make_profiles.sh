@@ -33,4 +33,9 @@ $NCU --set full --import-source on --replay-mode application -k regex:metro_gate
     -o "$OUT/gate_route_full" python tools/profile_target.py gate > "$OUT/gate_route_full.log" 2>&1
 full dispatch layout_kernel 5 python tools/profile_target.py dispatch
 full exchange metro_allgather_kernel 5 python tools/profile_target.py exchange
+full fused metro_ids_kernel 5 python tools/profile_target.py fused
+# the routing kernel with the caches NOT flushed between replays (steady state: the
+# ids, masks and the kernel's own code stay in L2) beside the default cold capture
+$NCU --set full --import-source on --cache-control none -k regex:metro_ids_kernel -s 5 -c 1 \
+    -o "$OUT/metro_cc_none_full" python tools/profile_target.py metro > "$OUT/metro_cc_none_full.log" 2>&1
 ls -la "$OUT"

@@ -13,7 +13,7 @@ import sys
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.environ.get("PROFILE_SRC") or os.path.join(REPO, "gpurun_out")
-DST = os.path.join(REPO, "profiles")
+DST = os.environ.get("PROFILE_DST") or os.path.join(REPO, "profiles")
 
 KEYS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -23,6 +23,11 @@ KEYS = [
     "launch__grid_size", "launch__block_size", "launch__cluster_dim_x", "launch__registers_per_thread",
     "launch__shared_mem_per_block_dynamic", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "smsp__inst_executed.sum", "lts__t_bytes.sum",
+    # where the DRAM reads come from: the SM's data path (ids, masks) vs the rest (instruction /
+    # constant fetch on a flushed cache)
+    "dram__sectors_read.sum", "lts__t_sectors_srcunit_tex_op_read.sum",
+    "lts__t_sectors_srcunit_tex_op_read_lookup_miss.sum", "lts__t_sectors_srcunit_tex_op_write.sum",
+    "smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio",
 ]
 
 
@@ -55,7 +60,8 @@ def main():
                       ("moe_gemm_fp8_down", "moe_fp8_down_full.ncu-rep"),
                       ("gate", "gate_full.ncu-rep"), ("gate_route", "gate_route_full.ncu-rep"),
                       ("dispatch", "dispatch_full.ncu-rep"),
-                      ("exchange", "exchange_full.ncu-rep")):
+                      ("exchange", "exchange_full.ncu-rep"), ("fused_route_layout", "fused_full.ncu-rep"),
+                      ("metro_cache_control_none", "metro_cc_none_full.ncu-rep")):
         path = os.path.join(SRC, rep)
         if not os.path.exists(path):
             continue
