@@ -680,9 +680,16 @@ static int hist_mode() {
 // (tools/cluster_sweep.py, DS / Q30 / Q235 shapes): one CTA is best below 8192
 // pairs (the exchange costs more than the split saves), 8-CTA clusters from
 // 8192 up to 32768 (at 8192 the two are within 0.1-0.2 us), 16 beyond.
-static int auto_cluster(int64_t num_pairs) {
+// Cluster size by batch (tools/cluster_sweep.py on B200, graph-replayed over a >L2
+// pool; profiles/r2_cluster_sweep.json): one CTA below 8192 pairs, 4 up to 16384
+// (DS B=1024: 7.23 vs 7.36 us at R=1 and 7.43 at R=8), 8 up to 65536 (B=8192:
+// 8.49 vs 8.86 at R=16), 16 beyond (the staged slice of one CTA is <= 65536 ids).
+// With the fused dispatch layout (more per-pair work after the decide phase) R = 8
+// stays ahead from 8192 pairs (DS B=1024: 8.9-9.0 vs 9.2 us at R = 4).
+static int auto_cluster(int64_t num_pairs, bool layout = false) {
     if (num_pairs < 8192) return 1;
-    if (num_pairs <= 32768) return 8;
+    if (num_pairs <= 16384) return layout ? 8 : 4;
+    if (num_pairs <= 65536) return 8;
     return 16;
 }
 
@@ -702,7 +709,7 @@ static int plan_ids(Kind kind, bool warp_hist, int64_t num_pairs, int N, int W, 
             return METRO_EARG;
         cands[nc++] = requested;
     } else {
-        for (int r = auto_cluster(num_pairs); r >= 1; r >>= 1) cands[nc++] = r;
+        for (int r = auto_cluster(num_pairs, lay_nrep > 0); r >= 1; r >>= 1) cands[nc++] = r;
     }
     for (int ci = 0; ci < nc; ++ci) {
         const int r = cands[ci];

@@ -634,10 +634,13 @@ static int launch_gemm(const void *W, int32_t E, int32_t M, int32_t K, const voi
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // persistent CTAs, round-robin items.  Balanced grid: the fewest CTAs that keep
     // the minimal number of waves (items per CTA), so every CTA gets the same item
-    // count (e.g. 2016 items: 144 CTAs x 14 instead of 148 with 92 x 14 + 56 x 13)
+    // count (e.g. 2016 items: 144 CTAs x 14 instead of 148 with 92 x 14 + 56 x 13).
+    // A/B on one B200 (tools/k3_grid_ab.sh): EPLB rank FFN -2 %, METRO rank within
+    // 0.4 %.  MOE_BALANCED_GRID=0 restores one CTA per SM.  (Device item counts --
+    // moe_grouped_gemm_dev -- are unknown here: one CTA per SM.)
     static const int balanced = [] {
         const char *v = getenv("MOE_BALANCED_GRID");
-        return v ? atoi(v) : 0;
+        return v ? atoi(v) : 1;
     }();
     int grid = num_ctas > 0 ? num_ctas : (n_items < sms ? n_items : sms);
     if (num_ctas <= 0 && balanced && n_items > sms && !n_items_dev) {
@@ -655,6 +658,7 @@ static int launch_gemm(const void *W, int32_t E, int32_t M, int32_t K, const voi
     prm.x_scale = x_scale;
     prm.mblocks = M / BM;
     prm.stamps = g_stamps;
+
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const bool narrow = max_item_tokens <= NarrowTile::kN;
     cudaError_t e;
