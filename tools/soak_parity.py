@@ -5,7 +5,8 @@ tally (the evidence under profiles/<round>_soak.json).
 
     python tools/soak_parity.py [--seconds 600] [--seed 1] [--out gpurun_out/soak.json]
 
-Entry points: METRO / EPLB routing from ids (every cluster size), METRO from
+Entry points: METRO / EPLB routing from ids (every cluster size; a quarter of the
+METRO calls through the eager launch plan, Router.bind), METRO from
 loads and from an order (metro-parallel), fused gating (cluster + whole GPU),
 dispatch layout (standalone and fused with METRO routing), the persistent host router, and the fused exchange with
 virtual ranks.  Instances: N 1..700 experts, G 1..128 ranks (multi-word masks),
@@ -65,7 +66,12 @@ def check_route(rng, ids, A):
     t = torch.from_numpy(np.ascontiguousarray(ids)).cuda()
     T = oracle.aggregate_loads(ids, A.shape[0])
     choice, counts, lam = oracle.route_metro(T, A)
-    o = Router(pl, "metro", cl).route(t).check()
+    rm = Router(pl, "metro", cl)
+    if rng.random() < 0.25 and ids.size > 0:
+        # the eager launch plan (metro_route_plan_create/launch_v1) instead of route()
+        o = rm.bind(t.reshape(-1))().check()
+    else:
+        o = rm.route(t).check()
     ok = (eq(o.loads.cpu(), T) and eq(o.choice.cpu(), choice) and eq(o.rank_counts.cpu(), counts)
           and int(o.lam.item()) == lam and eq(o.pair_rank.cpu().numpy().reshape(ids.shape),
                                               oracle.pair_rank_metro(ids, choice)))
