@@ -685,9 +685,12 @@ static int hist_mode() {
 // (DS B=1024: 7.23 vs 7.36 us at R=1 and 7.43 at R=8), 8 up to 65536 (B=8192:
 // 8.49 vs 8.86 at R=16), 16 beyond (the staged slice of one CTA is <= 65536 ids).
 // With the fused dispatch layout (more per-pair work after the decide phase) R = 8
-// stays ahead from 8192 pairs (DS B=1024: 8.9-9.0 vs 9.2 us at R = 4).
-static int auto_cluster(int64_t num_pairs, bool layout = false) {
+// stays ahead from 8192 pairs (DS B=1024: 8.9-9.0 vs 9.2 us at R = 4).  EPLB (the
+// comparison router) keeps round 1's policy: its per-pair occurrence ranks scale
+// with the slice of one CTA (B=8192: 14.7 us at R = 16 vs 22.5 at R = 8).
+static int auto_cluster(int64_t num_pairs, bool layout = false, bool eplb = false) {
     if (num_pairs < 8192) return 1;
+    if (eplb) return num_pairs <= 32768 ? 8 : 16;
     if (num_pairs <= 16384) return layout ? 8 : 4;
     if (num_pairs <= 65536) return 8;
     return 16;
@@ -709,7 +712,7 @@ static int plan_ids(Kind kind, bool warp_hist, int64_t num_pairs, int N, int W, 
             return METRO_EARG;
         cands[nc++] = requested;
     } else {
-        for (int r = auto_cluster(num_pairs, lay_nrep > 0); r >= 1; r >>= 1) cands[nc++] = r;
+        for (int r = auto_cluster(num_pairs, lay_nrep > 0, kind == kEplbIds); r >= 1; r >>= 1) cands[nc++] = r;
     }
     for (int ci = 0; ci < nc; ++ci) {
         const int r = cands[ci];
