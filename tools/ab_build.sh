@@ -1,6 +1,6 @@
 #!/usr/bin/env bash
 # Build a variant of libmetro_b200.so with extra nvcc flags into abtest/lib<NAME>.so
-# (A/B timing: tools/ab_libs.sh).  ./tools/ab_build.sh B "-DMETRO_OUT_TMA"
+# (A/B timing: tools/ab_libs.sh).  ./tools/ab_build.sh B "-DSOME_VARIANT_FLAG"
 set -eu
 name=$1; shift
 out=$PWD/abtest/build_$name
