@@ -47,6 +47,8 @@ def test_quality_fixture_reproduced_by_oracle(quality):
     assert np.array_equal(epl, quality["lam_eplb"])
     opt = quality["lam_opt"]
     assert (opt <= quality["lam_metro"]).all() and (quality["lam_metro"] <= quality["lam_eplb"]).all()
+    # the reference's own criterion on its own numbers (test_acceptance.py:86-88)
+    assert np.mean(quality["lam_metro"] / opt) <= 1.15 and np.mean(quality["lam_eplb"] / quality["lam_metro"]) >= 1.20
 
 
 @pytest.mark.gpu
