@@ -885,7 +885,6 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
             const int r = static_cast<int>(s_keys[c] >> 56);
             s_sid[rk] = e;
             if (try_packed) packed_entry(s_ent + rk * kES, r, s_mask[e], e);
-
             if (r == 2) atomicMax(&misc[M_N2], rk + 1);
             if (r <= 3) atomicMax(&misc[M_N3], rk + 1);  // end of the r=3 segment
         }
@@ -896,8 +895,6 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
             cta_sync();
             const int n2 = misc[M_N2];
             uint32_t *dlt = reinterpret_cast<uint32_t *>(smem + L.rpart);
-            // {dA_ij, c_ij = dA_ij - dB_ij} for ij = 01 02 03 12 13 23 (the round-1 layout
-            // with c in place of dA ^ dB): one thread per pair
             for (int q = tid; q < (n2 >> 2) * 6; q += kThreads) {
                 const int blk = q / 6, pr = q - blk * 6;
                 const int i = pr < 3 ? 0 : (pr < 5 ? 1 : 2);
