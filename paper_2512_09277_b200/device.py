@@ -87,12 +87,14 @@ class DevicePlacement:
         self.matrix = np.ascontiguousarray(mat, dtype=np.int8)
 
 
-@dataclass
+@dataclass(frozen=True)
 class RouteResult:
     """Device outputs of one routing launch (all int32 CUDA tensors).
 
     loads[N]; choice[N] (METRO; -1 inactive) or x[N, G] (EPLB); rank_counts[G];
     lam[1]; pair_rank[num_pairs] (optional); status[4] (see metro_route.h).
+    Frozen: Router.route() validates a reused result set once, so its tensors
+    cannot be swapped afterwards (the kernels write through raw pointers).
     """
 
     kind: str
