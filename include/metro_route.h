@@ -88,6 +88,7 @@ enum {
     METRO_EDIMS = -2,      /* N or G outside the supported range */
     METRO_ECUDA = -3,      /* CUDA launch / copy error (see metro_last_cuda_error) */
     METRO_ENOTBINARY = -4, /* placement matrix not binary */
+    METRO_ENOMEM = -5,     /* host allocation failed (launch plans) */
 };
 
 METRO_API int metro_abi_version(void);

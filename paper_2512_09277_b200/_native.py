@@ -30,6 +30,7 @@ EARG = -1
 EDIMS = -2
 ECUDA = -3
 ENOTBINARY = -4
+ENOMEM = -5
 HOST_ZEROCOPY = 1
 HOST_STABLE_BUFFERS = 2
 PLAN_METRO = 0

@@ -509,6 +509,15 @@ __device__ __forceinline__ uint4 lds4(const uint32_t *p) {
 __host__ __device__ constexpr uint32_t inc_lo(uint32_t g) { return g < 4 ? (1u << (8 * g)) : 0u; }
 __host__ __device__ constexpr uint32_t inc_hi(uint32_t g) { return g >= 4 ? (1u << (8 * (g - 4))) : 0u; }
 
+// Below this many replicated active experts (m2, an upper bound of the r = 2
+// steps) the greedy takes the r = 2 steps one at a time and the CTA skips the
+// block-of-four delta table (its pass + barrier cost more than the blocks save on
+// a short segment).  A/B on B200 (tools/ab_libs.sh, two boxes): Qwen3-30B shape
+// (m2 = 39) -0.08..-0.29 us per layer with single steps; DeepSeek-V3 B = 64
+// (m2 = 63..76) +0.03 us and B = 1024 (m2 = 85) +0.13..0.2 us, so they keep blocks.
+#ifndef METRO_R2_BLOCK_MIN
+#define METRO_R2_BLOCK_MIN 48
+#endif
 // Entry layouts (words):
 //   r=2  {selA, selB, incA_lo, incA_hi, xAB_lo, xAB_hi, ga | gb << 8, id}
 //   r=3  {selA, selB, selC, 0, incA_lo, incA_hi, xAB_lo, xAB_hi, incC_lo, incC_hi,
@@ -601,7 +610,17 @@ __device__ __forceinline__ PackedL packed_greedy(const Params &p, const uint32_t
         for (int i = 0; i < 4; ++i) choice[b[i].w] = static_cast<int32_t>((b[i].z >> (m[i] & 8u)) & 0xffu);
     };
     int s = 0;
-    if (n2 >= 4) {
+    if (m2 < METRO_R2_BLOCK_MIN) {  // one step at a time, the next entry prefetched (no delta table)
+        if (n2 > 0) {
+            uint4 a = lds4(ent), b = lds4(ent + 4);
+            for (; s < n2; ++s) {
+                const uint4 an = lds4(ent + (s + 1) * kES), bn = lds4(ent + (s + 1) * kES + 4);
+                step2(a, b);
+                a = an;
+                b = bn;
+            }
+        }
+    } else {
         uint4 a[4], b[4], d[3];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -888,10 +907,12 @@ __device__ bool metro_decide(const Params &p, const Layout &L, unsigned char *sm
             if (r == 2) atomicMax(&misc[M_N2], rk + 1);
             if (r <= 3) atomicMax(&misc[M_N3], rk + 1);  // end of the r=3 segment
         }
-        if (try_packed) {
+        if (try_packed && m2 >= METRO_R2_BLOCK_MIN) {
             // block-of-four corrections for the r=2 lookahead: for steps i < j of a
             // block with candidates (a_i, b_i), dX_ij = [b_j == X] - [a_j == X]; stored
-            // as {dA_ij, dA_ij - dB_ij} for ij = 01 02 03 12 13 23 (12 words per block)
+            // as {dA_ij, dA_ij - dB_ij} for ij = 01 02 03 12 13 23 (12 words per block).
+            // With fewer replicated experts (m2 < METRO_R2_BLOCK_MIN) the greedy steps
+            // one at a time and this pass and its barrier are skipped.
             cta_sync();
             const int n2 = misc[M_N2];
             uint32_t *dlt = reinterpret_cast<uint32_t *>(smem + L.rpart);

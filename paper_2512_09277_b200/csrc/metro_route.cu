@@ -37,6 +37,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <new>
 
 #include "../../include/dispatch_layout.h"
 #include "../../include/metro_route.h"
@@ -764,6 +765,7 @@ const char *metro_strerror(int code) {
         case METRO_EDIMS: return "unsupported dimensions (1 <= G <= 128, 1 <= N <= 4096) or shared memory exceeded";
         case METRO_ECUDA: return "CUDA error";
         case METRO_ENOTBINARY: return "placement matrix must be binary";
+        case METRO_ENOMEM: return "host memory allocation failed";
         default: return "unknown error";
     }
 }
@@ -904,8 +906,8 @@ int metro_route_plan_create_v1(int32_t kind, const int32_t *ids, int64_t num_pai
     else
         rc = METRO_EARG;
     if (rc) return rc;
-    *plan_out = new metro_route_plan(pl);
-    return METRO_OK;
+    *plan_out = new (std::nothrow) metro_route_plan(pl);  // no C++ exception across the C ABI
+    return *plan_out ? METRO_OK : METRO_ENOMEM;
 }
 
 int metro_route_plan_launch_v1(const metro_route_plan *pl, void *stream) {

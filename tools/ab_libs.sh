@@ -7,7 +7,7 @@ set -u
 libs=${1:-"A B"}
 for v in $libs; do
   METRO_B200_LIB=$PWD/abtest/lib$v.so timeout 300 python -m pytest -q -x tests/test_parity_gpu.py \
-      -k "golden or fuzz or max" 2>&1 | tail -1 | sed "s/^/$v parity: /"
+      -m gpu -k "golden or fuzz or max or baseline or fallback" 2>&1 | tail -1 | sed "s/^/$v parity: /"
 done
 for round in 1 2; do
   for v in $libs; do
