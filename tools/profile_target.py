@@ -1,6 +1,8 @@
 """Minimal launch sequences for ncu captures (no graphs, few launches).
 
     python tools/profile_target.py metro [B]     # 8 routing launches, DeepSeek-V3 shape
+    python tools/profile_target.py q30 [B]       # 8 routing launches, Qwen3-30B shape (128 experts: the
+                                                 # single-step r = 2 path), one CTA and a 4-CTA cluster
     python tools/profile_target.py eplb [B]      # 8 EPLB launches, same inputs
     python tools/profile_target.py gate [B]      # 8 fused gating top-k + METRO launches (fp32 scores)
     python tools/profile_target.py dispatch [B]  # 8 dispatch-layout launches behind METRO routing
@@ -29,7 +31,17 @@ def main():
     pl = DevicePlacement(A, dev)
     batches = [torch.from_numpy(gen_zipf_topk(256, 8, B, 1.2, 1000 + s, popularity_seed=7)).to(dev)
                for s in range(8)]
-    if what in ("metro", "eplb"):
+    if what == "q30":
+        A30 = make_placement(128, 8, 1.5, 7).matrix
+        pl30 = DevicePlacement(A30, dev)
+        for cl in (1, 4):
+            r = Router(pl30, "metro", cl)
+            out = r.alloc(B * 8, top_k=8)
+            for s in range(8):
+                ids = torch.from_numpy(gen_zipf_topk(128, 8, B, 1.2, 1000 + s, popularity_seed=7)).to(dev)
+                r.route(ids, out=out)
+            out.check()
+    elif what in ("metro", "eplb"):
         r = Router(pl, what)
         out = r.alloc(B * 8, top_k=8)
         for b in batches:

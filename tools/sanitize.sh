@@ -12,6 +12,9 @@ run() {  # label, tool, command...
 run "metro_ids_kernel (profile_target.py metro 256)" memcheck python tools/profile_target.py metro 256
 run "metro_ids_kernel" racecheck python tools/profile_target.py metro 256
 run "metro_ids_kernel" synccheck python tools/profile_target.py metro 256
+run "metro_ids_kernel, Qwen3-30B shape (q30 256: single r=2 steps)" memcheck python tools/profile_target.py q30 256
+run "metro_ids_kernel, Qwen3-30B shape (q30 256)" racecheck python tools/profile_target.py q30 256
+run "metro_ids_kernel, Qwen3-30B shape (q30 256)" synccheck python tools/profile_target.py q30 256
 run "eplb_ids_kernel (profile_target.py eplb 256)" racecheck python tools/profile_target.py eplb 256
 run "layout_kernel (profile_target.py dispatch 256)" racecheck python tools/profile_target.py dispatch 256
 run "layout_kernel" memcheck python tools/profile_target.py dispatch 256
