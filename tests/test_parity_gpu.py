@@ -202,6 +202,28 @@ def test_packed_greedy_fallback():
     check_metro(ids, A, 0)
 
 
+def test_r2_single_step_threshold():
+    """The packed greedy steps the r = 2 segment one at a time below
+    METRO_R2_BLOCK_MIN (48) replicated active experts and in blocks of four
+    (with the delta table) from 48 up: replicated-expert counts straddling the
+    threshold, every r = 2 segment length mod 4, mixes of r = 2 / 3 / >= 4."""
+    rng = np.random.default_rng(48)
+    n, g = 256, 8
+    for m in (0, 1, 2, 3, 4, 5, 31, 46, 47, 48, 49, 50, 51, 63, 64, 85, 120):
+        for trial in range(2):
+            A = np.zeros((n, g), dtype=np.int8)
+            A[np.arange(n), rng.integers(0, g, size=n)] = 1
+            multi = rng.choice(n, size=m, replace=False)
+            for e in multi:
+                r = int(rng.choice([2, 2, 2, 3, 4, 6]))
+                A[e, rng.choice(g, size=r, replace=False)] = 1
+                A[e] = np.minimum(A[e], 1)
+            ids = rng.integers(0, n, size=(1024, 8)).astype(np.int32)
+            ids[0] = np.arange(8)  # a few fixed ids; every expert is active at 8192 pairs w.h.p.
+            for cl in (0, 1, 4):
+                check_metro(ids, A, cl)
+
+
 def test_id_out_of_range_error():
     A = make_placement(128, 8, 1.5, 7).matrix
     ids = gen_zipf_topk(128, 8, 256, 1.2, 1)
