@@ -21,7 +21,7 @@ import torch
 
 from . import _native
 from .core import ValidationError
-from .device import DevicePlacement, RouteResult, Router, raise_status
+from .device import DevicePlacement, RouteResult, Router, _ptr, raise_status
 
 
 def replica_table(A) -> Tuple[np.ndarray, np.ndarray]:
@@ -148,7 +148,7 @@ class DispatchLayout:
         s = stream if stream is not None else torch.cuda.current_stream(pl.device)
         rc = _native.lib().metro_route_layout_v1(
             ids.data_ptr() if P else None, P, pl.mask.data_ptr(), pl.num_experts, pl.num_ranks,
-            self.rid_tab.data_ptr(), self.slot_base.data_ptr(), self.nrep, out.loads.data_ptr(),
+            self.rid_tab.data_ptr(), self.slot_base.data_ptr(), self.nrep, _ptr(out.loads),
             out.choice.data_ptr(), out.rank_counts.data_ptr(), out.lam.data_ptr(), out.pair_rank.data_ptr(),
             layout_out.pair_row.data_ptr(), layout_out.rep_off.data_ptr(), out.status.data_ptr(),
             self.cluster_ctas, ctypes.c_void_p(s.cuda_stream))

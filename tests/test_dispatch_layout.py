@@ -259,6 +259,23 @@ def test_fused_route_layout_fuzz_and_edges(_cuda):
 
 
 @pytest.mark.gpu
+def test_fused_route_layout_without_loads(_cuda):
+    """out.loads is optional on the fused route + layout, as on Router.route."""
+    import dataclasses
+
+    A = make_placement(256, 8, 1.5, 7).matrix
+    ids = torch.from_numpy(gen_zipf_topk(256, 8, 256, 1.2, 3, popularity_seed=7)).cuda()
+    pl = DevicePlacement(A)
+    lay = DispatchLayout(pl)
+    ref, ref_lo = lay.route_metro(ids)
+    out = dataclasses.replace(Router(pl, "metro").alloc(ids.numel(), top_k=8), loads=None)
+    got, lo = lay.route_metro(ids, out=out)
+    got.check()
+    assert torch.equal(got.choice, ref.choice) and torch.equal(got.pair_rank, ref.pair_rank)
+    assert torch.equal(lo.pair_row, ref_lo.pair_row) and torch.equal(lo.rep_off, ref_lo.rep_off)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("nrep", [31, 32, 33, 511, 512, 513, 1024])
 def test_fused_route_layout_replica_count_boundaries(_cuda, nrep):
     """rep_off has nrep + 1 entries: replica counts at the one-replica-per-thread
