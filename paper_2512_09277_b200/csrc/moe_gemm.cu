@@ -81,6 +81,7 @@ struct Params {
     int K;
     __nv_bfloat16 *Y;
     int ldy;
+    int rows;  // rows of X / Y: epilogue stores past it are dropped (memory-safety guard)
     int64_t *stamps;  // tuning only (moe_debug_set_stamps): per CTA {start ns, end ns}
 };
 
@@ -317,10 +318,11 @@ __global__ void __launch_bounds__(kThreads, 1) moe_gemm_kernel(const __grid_cons
                 // FP8: lane j fetches token c + j's activation scale once (issued before
                 // the TMEM load completes); every lane then takes it by shuffle
                 float sc = 1.0f;
-                if (FP8 && c + lane < item.n) sc = ws * __ldg(p.x_scale + item.t0 + c + lane);
+                if (FP8 && c + lane < item.n && item.t0 + c + lane < p.rows)
+                    sc = ws * __ldg(p.x_scale + item.t0 + c + lane);
                 TMEM_LD_X32(tbase + static_cast<uint32_t>(c), v);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                const int lim = min(32, item.n - c);
+                const int lim = min(min(32, item.n - c), p.rows - (item.t0 + c));
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
                     float y = __uint_as_float(v[j]);
@@ -654,6 +656,7 @@ static int launch_gemm(const void *W, int32_t E, int32_t M, int32_t K, const voi
     prm.K = K;
     prm.Y = static_cast<__nv_bfloat16 *>(Y);
     prm.ldy = M;
+    prm.rows = T;
     prm.w_scale = w_scale;
     prm.x_scale = x_scale;
     prm.mblocks = M / BM;

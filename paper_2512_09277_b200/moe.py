@@ -13,7 +13,7 @@ Expert FFN (DeepSeek-V3 geometry by default, bf16):
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import List, Sequence, Tuple
+from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 import torch
@@ -108,6 +108,25 @@ def _items_and_bound(items, max_item_tokens):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)), int(max_item_tokens)
 
 
+def _check_host_items(items: torch.Tensor, E: int, M: int, T: int) -> None:
+    """Host items must address existing experts, row blocks and token rows (the
+    kernel drops stores past T as a guard, but an item outside the problem is a
+    caller error)."""
+    if items.is_cuda or items.numel() == 0:
+        return
+    a = items.numpy()
+    e, mb, t0, n = a[:, 0], a[:, 1], a[:, 2], a[:, 3]
+    if (e < 0).any() or (e >= E).any() or (mb < 0).any() or (mb >= M // BM).any() or (t0 < 0).any() \
+            or (n < 0).any() or (t0.astype(np.int64) + n > T).any():
+        raise ValidationError("an item addresses an expert / row block / token range outside W and X")
+
+
+def _check_out(Y: Optional[torch.Tensor], T: int, M: int, device) -> None:
+    if Y is not None and (Y.dtype != torch.bfloat16 or Y.device != device or not Y.is_contiguous()
+                          or Y.dim() != 2 or tuple(Y.shape) != (T, M)):
+        raise ValidationError(f"Y must be a contiguous bfloat16 [{T}, {M}] tensor on {device}")
+
+
 def grouped_gemm(W: torch.Tensor, X: torch.Tensor, items, Y: torch.Tensor = None,
                  num_ctas: int = 0, max_item_tokens: int = None) -> torch.Tensor:
     """Y[t, m] = sum_k W[e][m, k] X[t, k] for every item (bf16 in/out, fp32 accumulate).
@@ -120,8 +139,12 @@ def grouped_gemm(W: torch.Tensor, X: torch.Tensor, items, Y: torch.Tensor = None
         raise ValidationError("W and X must be bfloat16")
     if W.dim() != 3 or X.dim() != 2 or W.shape[2] != X.shape[1]:
         raise ValidationError(f"shape mismatch: W {tuple(W.shape)}, X {tuple(X.shape)}")
+    if not (W.is_cuda and X.device == W.device and W.is_contiguous() and X.is_contiguous()):
+        raise ValidationError("W and X must be contiguous CUDA tensors on one device")
     E, M, K = W.shape
     T = X.shape[0]
+    _check_host_items(items, E, M, T)
+    _check_out(Y, T, M, W.device)
     items = items.to(device=W.device, dtype=torch.int32).contiguous()
     if Y is None:
         Y = torch.empty((T, M), dtype=torch.bfloat16, device=W.device)
@@ -229,9 +252,18 @@ def grouped_gemm_fp8(W8: torch.Tensor, w_scale: torch.Tensor, X8: torch.Tensor, 
     """Y[t, m] = w_scale[e, m / 128] * x_scale[t] * sum_k W8[e][m, k] X8[t, k] (E4M3 in, bf16 out)."""
     if W8.dtype != torch.uint8 or X8.dtype != torch.uint8:
         raise ValidationError("W8 and X8 must be E4M3 bytes (uint8)")
+    if W8.dim() != 3 or X8.dim() != 2 or W8.shape[2] != X8.shape[1]:
+        raise ValidationError(f"shape mismatch: W8 {tuple(W8.shape)}, X8 {tuple(X8.shape)}")
+    if not (W8.is_cuda and X8.device == W8.device and W8.is_contiguous() and X8.is_contiguous()):
+        raise ValidationError("W8 and X8 must be contiguous CUDA tensors on one device")
     E, M, K = W8.shape
     T = X8.shape[0]
+    for name, t, n in (("w_scale", w_scale, E * (M // BM)), ("x_scale", x_scale, T)):
+        if t.dtype != torch.float32 or t.device != W8.device or not t.is_contiguous() or t.numel() < n:
+            raise ValidationError(f"{name} must be a contiguous float32 tensor of >= {n} elements on {W8.device}")
     items, max_item_tokens = _items_and_bound(items, max_item_tokens)
+    _check_host_items(items, E, M, T)
+    _check_out(Y, T, M, W8.device)
     items = items.to(device=W8.device, dtype=torch.int32).contiguous()
     if Y is None:
         Y = torch.empty((T, M), dtype=torch.bfloat16, device=W8.device)

@@ -10,6 +10,7 @@ import pytest
 import torch
 
 from paper_2512_09277_b200 import moe
+from paper_2512_09277_b200.core import ValidationError
 
 pytestmark = pytest.mark.gpu
 RTOL = ATOL = 2e-2
@@ -289,3 +290,26 @@ def test_rank_moe_fp8_matches_host_plan():
         Yh = ffn.forward(X, torch.from_numpy(i1).to(dev), torch.from_numpy(i2).to(dev))
         torch.cuda.synchronize()
         torch.testing.assert_close(Y[:rows].float(), Yh.float(), rtol=0, atol=0)
+
+
+def test_grouped_gemm_rejects_items_and_outputs_outside_the_problem():
+    """Host items must address existing experts / row blocks / token rows, and a
+    caller's Y must be the [T, M] bf16 output (the kernel writes through raw
+    pointers; its epilogue also drops stores past T as a guard for device items)."""
+    dev = torch.device("cuda")
+    E, M, K, T = 2, 256, 128, 40
+    W = torch.zeros((E, M, K), dtype=torch.bfloat16, device=dev)
+    X = torch.zeros((T, K), dtype=torch.bfloat16, device=dev)
+    good = np.array([[0, 1, 0, 40]], dtype=np.int32)
+    moe.grouped_gemm(W, X, good)
+    for bad in ([[2, 0, 0, 8]], [[0, 2, 0, 8]], [[0, 0, 36, 8]], [[-1, 0, 0, 8]], [[0, 0, -1, 8]]):
+        with pytest.raises(ValidationError):
+            moe.grouped_gemm(W, X, np.array(bad, dtype=np.int32))
+    with pytest.raises(ValidationError):
+        moe.grouped_gemm(W, X, good, Y=torch.empty((T - 1, M), dtype=torch.bfloat16, device=dev))
+    # device items past T: the stores beyond row T are dropped, nothing else is touched
+    big = torch.full((T + 8, M), 7.0, dtype=torch.bfloat16, device=dev)
+    moe.grouped_gemm(W, X, torch.tensor([[0, 0, 32, 16]], dtype=torch.int32, device=dev),
+                     Y=big[:T], max_item_tokens=64)
+    torch.cuda.synchronize()
+    assert bool((big[T:] == 7.0).all()) and bool((big[32:T, :128] == 0).all())
