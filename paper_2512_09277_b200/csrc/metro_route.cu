@@ -25,7 +25,8 @@
 //       as an order-free prefix, replicated ones are stream-compacted and
 //       rank-sorted by the canonical key with broadcast loads; the serial greedy
 //       runs predicate-free in ONE thread on byte-packed counters for G <= 8
-//       (blocks of four r = 2 steps with precomputed corrections), else in one
+//       (blocks of four r = 2 steps with precomputed corrections; single steps
+//       below METRO_R2_BLOCK_MIN replicated experts), else in one
 //       warp (lane g owns L[g] << 8 | g; SEL -> redux.sync.min -> compare -> add);
 //   (E) each CTA writes pair_rank for its own slice from shared memory; CTA 0
 //       writes loads / choice / rank_counts / lam / status.
